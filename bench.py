@@ -1,0 +1,487 @@
+"""Benchmark: fused ACDC forward+backward rows/s at N=4096 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU, NCCL)
+
+A step is one pass of the hot path over one batch: forward (y = C3(d*C2(a*x)+b)),
+backward (dx and the three diagonal gradients, h2 recomputed), the fixed-order
+gradient reduction, and for N > 1 the NCCL all-reduce of the flat [ga|gd|gb]
+gradient buffer.  Batch 16384 rows per GPU (weak scaling).  Inputs are
+synthetic Gaussian fp32 tensors resident in HBM (each 256 MiB > the 126 MB
+L2, so no L2 flush is needed between steps).
+
+``--impl reference`` times the reference's own compiled CPU kernels
+(``oracle/_ref``, the Cython ``_kernels.pyx`` built from /root/reference) on
+this host's cores for the same metric, on a bounded row sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_FEAT = 4096
+BATCH = 16384
+METRIC = "ACDC fwd+bwd rows/sec at N=4096 (1/2/4/8 B200), % of HBM roofline"
+UNIT = "rows/s"
+BYTES_FWD = 8 * N_FEAT  # x in, y out (fp32)
+BYTES_BWD = 12 * N_FEAT  # x, dy in, dx out (h2 recomputed)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_FEAT)
+    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during timing."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._pump, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                power.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(smax) if smax else None,
+            "power_w_max": max(power) if power else None,
+            "samples": len(sm),
+            "reasons": sorted(reasons),
+        }
+
+
+# ------------------------------------------------------------- CPU baseline
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def reference_cpu(n, threads, rows, seconds=None, steps=None, warmup=0):
+    """Time the reference's compiled kernels (oracle/_ref) on host threads.
+
+    Returns (rows_per_s, kind, sample_desc, per_step_times)."""
+    from oracle import ref_kernels
+
+    rng = np.random.default_rng(0)
+    a, d = 1 + 0.1 * rng.standard_normal((2, n))
+    bias = 0.1 * rng.standard_normal(n)
+    x = rng.standard_normal((rows, n))
+    dy = rng.standard_normal((rows, n))
+    if ref_kernels.load() is not None:
+        layer = ref_kernels.RefAcdc(a, d, bias)
+        kind = "reference"
+
+        def step():
+            ref_kernels.fwd_bwd_threaded(layer, x, dy, threads)
+    else:  # the numpy restatement (fp64) as a port
+        from oracle import acdc_oracle as O
+
+        kind = "port"
+        threads = 1
+
+        def step():
+            y, h2 = O.acdc_forward(x, a, d, bias)
+            O.acdc_backward(x, h2, dy, a, d)
+    for _ in range(warmup):
+        step()
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+        if steps is not None and len(times) >= steps:
+            break
+        if steps is None and time.perf_counter() - t_start >= seconds:
+            break
+    total = sum(times)
+    rps = rows * len(times) / total
+    sample = (f"{len(times)} x fwd+bwd of {rows} rows at N={n}, fp64 (reference dtype), "
+              f"{threads} host threads, {cpu_model()}")
+    return rps, kind, sample, times, threads
+
+
+# ------------------------------------------------------------------ our arm
+def dist_setup(gpus):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(v, world):
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1511_05946_b200 import functional as F
+
+    world, rank, local = dist_setup(args.gpus)
+    n, B = args.n, args.batch
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    x = torch.randn(B, n, device=dev, generator=g)
+    dy = torch.randn(B, n, device=dev, generator=g)
+    a = 1 + 0.1 * torch.randn(n, device=dev, generator=g)
+    d = 1 + 0.1 * torch.randn(n, device=dev, generator=g)
+    bias = 0.1 * torch.randn(n, device=dev, generator=g)
+    if world > 1:  # replicated parameters
+        for p in (a, d, bias):
+            dist.broadcast(p, 0)
+    grads = torch.zeros(3, n, device=dev)
+    y = torch.empty_like(x)
+    dx = torch.empty_like(x)
+    F.prepare(n, dev)
+    stream = torch.cuda.current_stream()
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+
+    def step(i=None):
+        e = ev[i] if i is not None else None
+        if e: e[0].record(stream)
+        F.acdc_forward(x, a, d, bias, out=y)
+        if e: e[1].record(stream)
+        F.acdc_backward(x, dy, a, d, grads[0], grads[1], grads[2], accumulate=False, out=dx)
+        if e: e[2].record(stream)
+        if world > 1:
+            dist.all_reduce(grads)
+        if e: e[3].record(stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier(world)
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.15)
+    barrier(world)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    t1.record(stream)
+    barrier(world)
+    clocks = sampler.stop()
+    elapsed_ms = t0.elapsed_time(t1)
+    fwd_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps
+    bwd_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
+    ar_ms = sum(e[2].elapsed_time(e[3]) for e in ev) / args.steps
+    max_ms = max_over_ranks(elapsed_ms, world)
+    ms_per_step = max_ms / args.steps
+    value = world * B * args.steps / (max_ms / 1e3)
+
+    # e2e through the public API with host buffers (pinned), copies in the timed region
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_measure(F, n, B, a, d, bias, dev, world, steps=max(3, min(args.steps, 10)))
+
+    dense = None
+    if not args.no_dense and rank == 0:
+        dense = dense_measure(n, B, dev)
+
+    out = None
+    if rank == 0:
+        hbm, src = peaks()
+        # dominant kernel = the longer of fwd / bwd (bwd: acdc_bwd_kernel + grad reduce)
+        if bwd_ms >= fwd_ms:
+            kname, kms, kbytes = "acdc_bwd_kernel(+grad_reduce)", bwd_ms, BYTES_BWD * n // N_FEAT * B
+        else:
+            kname, kms, kbytes = "acdc_fwd_kernel", fwd_ms, BYTES_FWD * n // N_FEAT * B
+        achieved = kbytes / (kms / 1e3) / 1e9
+        step_bytes = (BYTES_FWD + BYTES_BWD) * n // N_FEAT * B
+        step_gbs = step_bytes / ((fwd_ms + bwd_ms) / 1e3) / 1e9
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get(kname.split("(")[0])
+            except Exception:
+                traffic = None
+        out = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": max(args.warmup, 3),
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic Gaussian x, dy ~ N(0,1); a, d ~ N(1, 0.1^2); bias ~ N(0, 0.1^2)",
+            "config": {
+                "workload": f"single ACDC layer fwd+bwd, N={n}, batch {B} rows per GPU, fp32",
+                "n": n,
+                "rows_per_gpu": B,
+                "global_rows": B * world,
+                "parallelism": f"dp{world}" if world > 1 else "single",
+                "l2": "inputs larger than L2 (x, dy, y, dx are 256 MiB each); no flush",
+            },
+            "roofline": {
+                "kernel": kname,
+                "bound": "hbm",
+                "achieved": achieved,
+                "peak": hbm,
+                "peak_source": src,
+                "unit": "GB/s",
+                "frac": achieved / hbm,
+                "traffic": traffic,
+                "algorithmic_bytes_per_launch": kbytes,
+                "avg_launch_ms": kms,
+            },
+            "roofline_step": {
+                "bytes_per_row": (BYTES_FWD + BYTES_BWD) * n // N_FEAT,
+                "achieved_gbs": step_gbs,
+                "frac": step_gbs / hbm,
+                "fwd_ms": fwd_ms,
+                "bwd_ms": bwd_ms,
+                "allreduce_ms": ar_ms,
+            },
+            "clocks": clocks,
+            "gpu_launches": 3 * args.steps,
+            "e2e": e2e,
+            "dense_cublas": dense,
+        }
+        if not args.no_cpu_baseline and world == 1:
+            thr = cpu_threads()
+            rows = max(1024, 64 * thr)
+            rps, kind, sample, _, used = reference_cpu(n, thr, rows, seconds=12.0, warmup=1)
+            out["cpu_baseline"] = {"value": rps, "unit": UNIT, "cores": used, "kind": kind, "sample": sample}
+    if world > 1:
+        dist.destroy_process_group()
+    return out
+
+
+def e2e_measure(F, n, B, a, d, bias, dev, world, steps):
+    """Rows/s through the public API with pinned host buffers: H2D x, dy;
+    forward; backward; D2H dx and grads — all inside the timed region."""
+    import torch
+    import torch.distributed as dist
+
+    xh = torch.randn(B, n).pin_memory()
+    dyh = torch.randn(B, n).pin_memory()
+    dxh = torch.empty(B, n).pin_memory()
+    gh = torch.empty(3, n).pin_memory()
+    grads = torch.zeros(3, n, device=dev)
+    xd = torch.empty(B, n, device=dev)
+    dyd = torch.empty(B, n, device=dev)
+
+    def step():
+        xd.copy_(xh, non_blocking=True)
+        dyd.copy_(dyh, non_blocking=True)
+        F.acdc_forward(xd, a, d, bias)
+        dx = F.acdc_backward(xd, dyd, a, d, grads[0], grads[1], grads[2], accumulate=False)
+        if world > 1:
+            dist.all_reduce(grads)
+        dxh.copy_(dx, non_blocking=True)
+        gh.copy_(grads, non_blocking=True)
+
+    step()
+    barrier(world)
+    s = torch.cuda.current_stream()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(s)
+    for _ in range(steps):
+        step()
+    t1.record(s)
+    barrier(world)
+    ms = max_over_ranks(t0.elapsed_time(t1), world)
+    return {
+        "value": world * B * steps / (ms / 1e3),
+        "unit": UNIT,
+        "h2d_bytes_per_step": 2 * B * n * 4,
+        "d2h_bytes_per_step": B * n * 4 + 3 * n * 4,
+        "steps": steps,
+        "path": "functional.acdc_forward/acdc_backward (C ABI) with pinned host x, dy -> dx, grads",
+    }
+
+
+def dense_measure(n, B, dev):
+    """cuBLAS dense linear of the same N, fwd + bwd (dX and dW), fp32, TF32 off and on."""
+    import torch
+
+    res = {}
+    w = torch.randn(n, n, device=dev) / math.sqrt(n)
+    x = torch.randn(B, n, device=dev)
+    gy = torch.randn(B, n, device=dev)
+    for tf32 in (False, True):
+        torch.backends.cuda.matmul.allow_tf32 = tf32
+        def step():
+            y = x @ w
+            gx = gy @ w.t()
+            gw = x.t() @ gy
+            return y, gx, gw
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        e0.record()
+        for _ in range(reps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        res["tf32" if tf32 else "fp32"] = {"rows_per_s": B / (ms / 1e3), "ms_per_step": ms,
+                                            "tflops": 6 * B * n * n / (ms / 1e3) / 1e12}
+    torch.backends.cuda.matmul.allow_tf32 = False
+    return res
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    thr = cpu_threads()
+    rows = max(512, 32 * thr)
+    rps, kind, sample, times, used = reference_cpu(args.n, thr, rows, steps=args.steps, warmup=args.warmup)
+    ms = 1e3 * sum(times) / len(times)
+    return {
+        "metric": METRIC,
+        "value": rps,
+        "unit": UNIT,
+        "impl": "reference",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic Gaussian",
+        "config": {"workload": f"single ACDC layer fwd+bwd, N={args.n}, reference CPU path on {rows}-row samples",
+                   "n": args.n, "rows_per_step": rows},
+        "cpu_baseline": {"value": rps, "unit": UNIT, "cores": used, "kind": kind, "sample": sample},
+        "e2e": {"value": rps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        out = run_reference(args)
+    else:
+        out = run_ours(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

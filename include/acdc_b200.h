@@ -1,0 +1,89 @@
+/*
+ * acdc_b200.h — C ABI of the B200-native ACDC structured-linear-layer kernels.
+ *
+ * Drop-in boundary for the reference package's forward / backward /
+ * parameter-gradient hot path (reference: /root/reference/pkg/src/acdc).
+ * Every entry point takes plain device pointers, sizes and a CUDA stream
+ * handle; no torch or numpy types cross this boundary.  The library never
+ * allocates or frees caller memory (the only library-owned device memory is
+ * a per-device, per-N cache of fp32 twiddle tables, built from fp64 on first
+ * use or by acdc_prepare).
+ *
+ * Conventions
+ *   - fp32 row-major matrices: row r of x starts at x + r*ldx (ldx >= n).
+ *   - n is a power of two, 1 <= n <= acdc_max_n() (32768).
+ *   - Calls are stream-ordered and asynchronous; the library keeps no mutable
+ *     per-call state, so calls on distinct streams from distinct host threads
+ *     are safe.  Call acdc_prepare(n) before CUDA-graph capture.
+ *   - Return 0 on success or a negative ACDC_E_* code; acdc_strerror(code)
+ *     gives the message (for ACDC_E_SIZE it is the reference's ValueError text,
+ *     transforms.py:96-97).
+ *
+ * Reference interface each entry point replaces (file:line under pkg/src/acdc):
+ *   acdc_fwd_f32   AcdcLayer.forward                 layers.py:141-146
+ *   acdc_bwd_f32   AcdcLayer.backward (accumulates)  layers.py:148-156
+ *   acdc_dct2_f32  dct(plan, x)  / kernels.dct2_batch transforms.py:137-145, _kernels.pyx:60-73
+ *   acdc_dct3_f32  idct(plan, y) / kernels.dct3_batch transforms.py:148-156, _kernels.pyx:76-91
+ *   acdc_prepare   DctPlan(n, mode="fast") table build transforms.py:86-122
+ */
+#ifndef ACDC_B200_H
+#define ACDC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ACDC_ABI_VERSION 1
+
+#define ACDC_OK 0
+#define ACDC_E_SIZE (-1)  /* n not a power of two, or n > acdc_max_n()  (ValueError) */
+#define ACDC_E_SHAPE (-2) /* rows < 0 or ld < n                          (ValueError) */
+#define ACDC_E_ALIGN (-3) /* misaligned pointer                          (ValueError) */
+#define ACDC_E_WS (-4)    /* workspace missing or too small              (ValueError) */
+#define ACDC_E_CUDA (-5)  /* CUDA launch / runtime failure               (RuntimeError) */
+#define ACDC_E_NULL (-6)  /* required pointer is NULL                    (ValueError) */
+
+/* cudaStream_t without requiring cuda_runtime.h (0 = legacy default stream). */
+typedef struct CUstream_st* acdc_stream_t;
+
+int acdc_abi_version(void);
+const char* acdc_strerror(int code);
+const char* acdc_last_error(void);
+int acdc_max_n(void);
+
+/* Build the twiddle tables and launch configuration for size n on the current
+ * device (the DctPlan constructor, transforms.py:86-122).  Synchronous. */
+int acdc_prepare(int32_t n);
+
+/* y = C3(d * C2(a * x) + bias) row-wise; C2 = orthonormal DCT-II, C3 its
+ * inverse (layers.py:141-146).  x, y: [rows, n]; a, d, bias: [n]. */
+int acdc_fwd_f32(const float* x, float* y, const float* a, const float* d, const float* bias, int64_t rows,
+                 int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream);
+
+/* Bytes of scratch acdc_bwd_f32 needs for (rows, n) on the current device
+ * (per-group gradient partials; 0 on error). */
+size_t acdc_bwd_workspace_bytes(int64_t rows, int32_t n);
+
+/* Backward of acdc_fwd_f32 (layers.py:148-156), h2 recomputed:
+ *   g3 = C2(dy); g1 = C3(d * g3); dx = a * g1
+ *   grad_bias (+)= sum_rows g3; grad_d (+)= sum_rows C2(a*x) * g3; grad_a (+)= sum_rows x * g1
+ * accumulate != 0 adds into the existing grads (the reference's "+="),
+ * accumulate == 0 overwrites them.  The batch reduction is deterministic
+ * (fixed-order, fp64 second pass): identical inputs give bitwise-identical
+ * gradients on the same device. */
+int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, const float* d, float* grad_a,
+                 float* grad_d, float* grad_bias, int accumulate, void* ws, size_t ws_bytes, int64_t rows,
+                 int32_t n, int64_t ldx, int64_t ldy, int64_t lddx, acdc_stream_t stream);
+
+/* Row-wise orthonormal DCT-II / DCT-III (the reference dct / idct). */
+int acdc_dct2_f32(const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream);
+int acdc_dct3_f32(const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ACDC_B200_H */

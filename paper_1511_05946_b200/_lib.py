@@ -1,0 +1,83 @@
+"""ctypes binding of ``libacdc_b200.so`` (the C ABI in ``include/acdc_b200.h``).
+
+There is no fallback: if the library is missing or cannot be loaded, every
+call raises.  Error codes map to the exception types the reference raises for
+the same conditions (``ValueError`` for size/shape problems, ``RuntimeError``
+for CUDA failures; transforms.py:96-97, layers.py:91-97).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libacdc_b200.so")
+
+ACDC_OK = 0
+ACDC_E_SIZE = -1
+ACDC_E_SHAPE = -2
+ACDC_E_ALIGN = -3
+ACDC_E_WS = -4
+ACDC_E_CUDA = -5
+ACDC_E_NULL = -6
+
+ABI_VERSION = 1
+
+# name -> (restype, argtypes)
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+SIGNATURES = {
+    "acdc_abi_version": (ctypes.c_int, []),
+    "acdc_strerror": (ctypes.c_char_p, [ctypes.c_int]),
+    "acdc_last_error": (ctypes.c_char_p, []),
+    "acdc_max_n": (ctypes.c_int, []),
+    "acdc_prepare": (ctypes.c_int, [_I32]),
+    "acdc_fwd_f32": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I32, _I64, _I64, _P]),
+    "acdc_bwd_workspace_bytes": (ctypes.c_size_t, [_I64, _I32]),
+    "acdc_bwd_f32": (
+        ctypes.c_int,
+        [_P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _I64, _I32, _I64, _I64, _I64, _P],
+    ),
+    "acdc_dct2_f32": (ctypes.c_int, [_P, _P, _I64, _I32, _I64, _I64, _P]),
+    "acdc_dct3_f32": (ctypes.c_int, [_P, _P, _I64, _I32, _I64, _I64, _P]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load():
+    """Load (once) and return the ctypes library; raises if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_1511_05946_b200.build` "
+                "(there is no CPU fallback)"
+            )
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        ver = lib.acdc_abi_version()
+        if ver != ABI_VERSION:
+            raise RuntimeError(f"libacdc_b200 ABI {ver} != expected {ABI_VERSION}")
+        _lib = lib
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == ACDC_OK:
+        return
+    msg = load().acdc_strerror(rc).decode()
+    if rc == ACDC_E_CUDA:
+        raise RuntimeError(msg)
+    raise ValueError(msg)

@@ -1,0 +1,167 @@
+"""Tensor-level entry points over the C ABI, plus the autograd Function.
+
+Every op launches on ``torch.cuda.current_stream()`` of the input's device and
+returns without synchronising.  Inputs must be CUDA fp32 tensors whose rows
+are contiguous (stride(-1) == 1); anything else is made contiguous first.
+
+Reference counterparts (under /root/reference/pkg/src/acdc):
+  acdc_forward   AcdcLayer.forward   layers.py:141-146
+  acdc_backward  AcdcLayer.backward  layers.py:148-156 (accumulating grads)
+  dct / idct     transforms.py:137-156
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+__all__ = ["acdc_forward", "acdc_backward", "dct", "idct", "AcdcFunction", "acdc", "prepare"]
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def _rows2d(x: torch.Tensor, n: int, name: str = "x") -> torch.Tensor:
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if x.dim() != 2 or x.shape[1] != n:
+        raise ValueError(f"{name} must have shape (batch, {n}), got {tuple(x.shape)}")
+    if x.dtype != torch.float32:
+        x = x.float()
+    if x.stride(1) != 1 or (x.shape[0] > 1 and x.stride(0) < n):
+        x = x.contiguous()
+    return x
+
+
+def _vec(v: torch.Tensor, n: int, dev, name: str) -> torch.Tensor:
+    if v.dim() != 1 or v.shape[0] != n:
+        raise ValueError(f"{name} must have shape ({n},), got {tuple(v.shape)}")
+    if v.device != dev or v.dtype != torch.float32 or not v.is_contiguous():
+        v = v.to(device=dev, dtype=torch.float32).contiguous()
+    return v
+
+
+def _ld(x: torch.Tensor, n: int) -> int:
+    return x.stride(0) if x.shape[0] > 1 else n
+
+
+def prepare(n: int, device=None) -> None:
+    """Build tables and launch configuration for size n (call before graph capture)."""
+    with torch.cuda.device(device if device is not None else torch.cuda.current_device()):
+        _lib.check(_lib.load().acdc_prepare(int(n)))
+
+
+def acdc_forward(x: torch.Tensor, a: torch.Tensor, d: torch.Tensor, bias: torch.Tensor, out=None) -> torch.Tensor:
+    """y = C3(d * C2(a * x) + bias) row-wise (layers.py:141-146)."""
+    n = a.shape[0]
+    x = _rows2d(x, n)
+    dev = x.device
+    a, d, bias = (_vec(v, n, dev, nm) for v, nm in ((a, "a"), (d, "d"), (bias, "bias")))
+    y = torch.empty_like(x, memory_format=torch.contiguous_format) if out is None else out
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        _lib.check(
+            lib.acdc_fwd_f32(_ptr(x), _ptr(y), _ptr(a), _ptr(d), _ptr(bias), x.shape[0], n, _ld(x, n), _ld(y, n),
+                             _stream(x))
+        )
+    return y
+
+
+def acdc_backward(
+    x: torch.Tensor,
+    dy: torch.Tensor,
+    a: torch.Tensor,
+    d: torch.Tensor,
+    grad_a: torch.Tensor,
+    grad_d: torch.Tensor,
+    grad_bias: torch.Tensor,
+    accumulate: bool = True,
+    out=None,
+) -> torch.Tensor:
+    """dx and (accumulated) parameter gradients of acdc_forward (layers.py:148-156).
+
+    grad_a / grad_d / grad_bias are CUDA fp32 (n,) tensors updated in place:
+    ``+=`` when ``accumulate`` (the reference contract), ``=`` otherwise.
+    """
+    n = a.shape[0]
+    x = _rows2d(x, n)
+    dy = _rows2d(dy, n, "grad_y")
+    if dy.shape[0] != x.shape[0]:
+        raise ValueError(f"grad_y has {dy.shape[0]} rows, input had {x.shape[0]}")
+    dev = x.device
+    a, d = _vec(a, n, dev, "a"), _vec(d, n, dev, "d")
+    for g in (grad_a, grad_d, grad_bias):
+        if g.device != dev or g.dtype != torch.float32 or not g.is_contiguous() or g.shape != (n,):
+            raise ValueError("gradient buffers must be contiguous fp32 (n,) tensors on the input device")
+    dx = torch.empty_like(x, memory_format=torch.contiguous_format) if out is None else out
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        wsb = lib.acdc_bwd_workspace_bytes(x.shape[0], n)
+        if wsb == 0:
+            _lib.check(_lib.ACDC_E_CUDA)
+        ws = torch.empty((wsb + 3) // 4, dtype=torch.float32, device=dev)
+        _lib.check(
+            lib.acdc_bwd_f32(
+                _ptr(x), _ptr(dy), _ptr(dx), _ptr(a), _ptr(d), _ptr(grad_a), _ptr(grad_d), _ptr(grad_bias),
+                1 if accumulate else 0, _ptr(ws), wsb, x.shape[0], n, _ld(x, n), _ld(dy, n), _ld(dx, n), _stream(x),
+            )
+        )
+    return dx
+
+
+def _transform(fn_name: str, x: torch.Tensor) -> torch.Tensor:
+    squeeze = x.dim() == 1
+    if squeeze:
+        x = x.unsqueeze(0)
+    if x.dim() != 2:
+        raise ValueError(f"expected 1-D or 2-D input, got shape {tuple(x.shape)}")
+    n = x.shape[1]
+    x = _rows2d(x, n)
+    y = torch.empty_like(x, memory_format=torch.contiguous_format)
+    lib = _lib.load()
+    with torch.cuda.device(x.device):
+        _lib.check(getattr(lib, fn_name)(_ptr(x), _ptr(y), x.shape[0], n, _ld(x, n), _ld(y, n), _stream(x)))
+    return y[0] if squeeze else y
+
+
+def dct(x: torch.Tensor) -> torch.Tensor:
+    """Row-wise orthonormal DCT-II (transforms.py:137-145)."""
+    return _transform("acdc_dct2_f32", x)
+
+
+def idct(x: torch.Tensor) -> torch.Tensor:
+    """Row-wise orthonormal DCT-III, the inverse of :func:`dct` (transforms.py:148-156)."""
+    return _transform("acdc_dct3_f32", x)
+
+
+class AcdcFunction(torch.autograd.Function):
+    """Autograd wrapper: forward = acdc_fwd_f32, backward = acdc_bwd_f32 with h2
+    recomputed; parameter grads are returned (accumulate=False)
+    and summed into ``.grad`` by autograd."""
+
+    @staticmethod
+    def forward(ctx, x, a, d, bias):
+        y = acdc_forward(x, a, d, bias)
+        ctx.save_for_backward(x, a, d)
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, a, d = ctx.saved_tensors
+        n = a.shape[0]
+        ga = torch.empty(n, dtype=torch.float32, device=x.device)
+        gd = torch.empty_like(ga)
+        gb = torch.empty_like(ga)
+        dx = acdc_backward(x, gy, a, d, ga, gd, gb, accumulate=False)
+        return dx, ga, gd, gb
+
+
+def acdc(x, a, d, bias):
+    """Differentiable ACDC layer: ``AcdcFunction.apply``."""
+    return AcdcFunction.apply(x, a, d, bias)

@@ -1,0 +1,340 @@
+"""Drop-in mirror of the reference layer API (``acdc.layers``) on B200 kernels.
+
+Same constructors, methods, attribute names and error behaviour as
+``/root/reference/pkg/src/acdc/layers.py``; the numerics run through the
+sm_100a kernels (``functional.py`` -> ``libacdc_b200.so``), in fp32.
+
+* Inputs may be CUDA tensors (kept on device; the result is a CUDA tensor) or
+  host arrays / tensors (copied to the layer's device; the result comes back
+  as a float64 numpy array, like the reference).
+* Parameters (``a``, ``d``, ``bias_d``) and gradient accumulators are fixed
+  CUDA fp32 storage updated in place (layers.py:14-15); ``backward``
+  accumulates into the gradients (layers.py:152-155) until ``zero_grads``.
+* ``backward`` before ``forward`` raises ``RuntimeError`` and consumes the
+  cache unless ``retain_cache`` (layers.py:99-105).
+* The layer caches only ``x``; ``h2`` is recomputed inside the fused backward
+  kernel instead of being stored (layers.py:145).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import functional as F
+
+__all__ = [
+    "Param",
+    "Layer",
+    "AcdcLayer",
+    "ReluLayer",
+    "PermutationLayer",
+    "DenseLayer",
+    "Cascade",
+    "acdc_cascade",
+    "count_params",
+]
+
+
+def _is_pow2(n: int) -> bool:
+    return n > 0 and (n & (n - 1)) == 0
+
+
+def _device(device) -> torch.device:
+    if device is None:
+        if not torch.cuda.is_available():
+            raise RuntimeError("the b200 backend needs a CUDA device (there is no CPU fallback)")
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+@dataclass
+class Param:
+    """One trainable tensor plus its gradient accumulator (layers.py:50-63)."""
+
+    name: str
+    value: torch.Tensor
+    grad: torch.Tensor
+    decay: bool = False
+    lr_mult: float = 1.0
+
+
+class Layer:
+    """Common interface: forward, backward, parameter access (layers.py:66-105)."""
+
+    linear = True
+    complex_domain = False
+    n_in: int
+    n_out: int
+    device: torch.device
+
+    def forward(self, x):
+        raise NotImplementedError
+
+    def backward(self, grad_y, retain_cache=False):
+        raise NotImplementedError
+
+    def params(self):
+        return []
+
+    def param_count(self):
+        return 0
+
+    def zero_grads(self):
+        for p in self.params():
+            p.grad.zero_()
+
+    # -- input handling (layers.py:91-97): 2-D (batch, n_in) or ValueError
+    def _check_input(self, x, dtype=torch.float32):
+        host = not (isinstance(x, torch.Tensor) and x.is_cuda)
+        if isinstance(x, torch.Tensor):
+            t = x
+        else:
+            t = torch.as_tensor(np.asarray(x))
+        if t.dim() != 2 or t.shape[1] != self.n_in:
+            raise ValueError(
+                f"{type(self).__name__} expects (batch, {self.n_in}) input, got shape {tuple(t.shape)}"
+            )
+        if host:
+            t = t.to(dtype=dtype).pin_memory().to(self.device, non_blocking=True) if t.numel() else t.to(
+                self.device, dtype=dtype)
+        elif t.dtype != dtype or t.device != self.device:
+            t = t.to(device=self.device, dtype=dtype)
+        return t.contiguous(), host
+
+    def _take_cache(self, retain):
+        if getattr(self, "_cache", None) is None:
+            raise RuntimeError(f"{type(self).__name__}.backward called before forward")
+        cache = self._cache
+        if not retain:
+            self._cache = None
+        return cache
+
+    @staticmethod
+    def _out(y: torch.Tensor, host: bool):
+        if not host:
+            return y
+        return y.detach().to("cpu", dtype=torch.float64).numpy()
+
+
+class AcdcLayer(Layer):
+    """Diagonal, DCT, diagonal-with-bias, inverse DCT (layers.py:108-156).
+
+    ``backend`` accepts the reference values ("auto", "compiled", "python")
+    plus "b200"; all of them run the B200 kernels here.  ``dct_mode`` "naive"
+    is accepted for API parity and computes the same orthonormal transform.
+    """
+
+    def __init__(self, n, dct_mode="fast", backend="auto", device=None):
+        if dct_mode not in ("naive", "fast"):
+            raise ValueError(f"unknown DCT mode {dct_mode!r}, expected one of ('naive', 'fast')")
+        if not _is_pow2(n):
+            raise ValueError(f"fast DCT requires a power-of-two size, got {n}")
+        self.n_in = self.n_out = n
+        self.dct_mode = dct_mode
+        self.backend = backend
+        self.device = _device(device)
+        kw = dict(dtype=torch.float32, device=self.device)
+        self.a = torch.ones(n, **kw)
+        self.d = torch.ones(n, **kw)
+        self.bias_d = torch.zeros(n, **kw)
+        self.grad_a = torch.zeros(n, **kw)
+        self.grad_d = torch.zeros(n, **kw)
+        self.grad_bias_d = torch.zeros(n, **kw)
+        self._params = [
+            Param("a", self.a, self.grad_a),
+            Param("d", self.d, self.grad_d),
+            Param("bias_d", self.bias_d, self.grad_bias_d),
+        ]
+        self._cache = None
+        F.prepare(n, self.device)
+
+    @property
+    def n(self):
+        return self.n_in
+
+    def params(self):
+        return self._params
+
+    def param_count(self):
+        return 3 * self.n_in
+
+    def forward(self, x):
+        x, host = self._check_input(x)
+        y = F.acdc_forward(x, self.a, self.d, self.bias_d)
+        self._cache = x
+        return self._out(y, host)
+
+    def backward(self, grad_y, retain_cache=False):
+        x = self._take_cache(retain_cache)
+        gy, host = self._check_input(grad_y)
+        if gy.shape[0] != x.shape[0]:
+            raise ValueError(f"grad_y has {gy.shape[0]} rows, forward input had {x.shape[0]}")
+        dx = F.acdc_backward(x, gy, self.a, self.d, self.grad_a, self.grad_d, self.grad_bias_d, accumulate=True)
+        return self._out(dx, host)
+
+
+class ReluLayer(Layer):
+    """max(x, 0) with the strict ``x > 0`` mask (layers.py:218-233)."""
+
+    linear = False
+
+    def __init__(self, n, device=None):
+        self.n_in = self.n_out = n
+        self.device = _device(device)
+        self._cache = None
+
+    def forward(self, x):
+        x, host = self._check_input(x)
+        self._cache = x > 0
+        return self._out(torch.clamp_min(x, 0.0), host)
+
+    def backward(self, grad_y, retain_cache=False):
+        mask = self._take_cache(retain_cache)
+        gy, host = self._check_input(grad_y)
+        return self._out(gy * mask, host)
+
+
+class PermutationLayer(Layer):
+    """Fixed permutation of the feature axis (layers.py:236-265)."""
+
+    def __init__(self, n, perm=None, rng=None, device=None):
+        self.n_in = self.n_out = n
+        self.device = _device(device)
+        if perm is None:
+            if rng is None:
+                raise ValueError("PermutationLayer needs an explicit perm or an rng")
+            perm = rng.permutation(n)
+        perm = np.asarray(perm.cpu() if isinstance(perm, torch.Tensor) else perm, dtype=np.int64)
+        if sorted(perm.tolist()) != list(range(n)):
+            raise ValueError("perm is not a bijection on 0..n-1")
+        self.perm = perm
+        self.inverse_perm = np.argsort(perm)
+        self._perm_t = torch.as_tensor(perm, device=self.device)
+        self._inv_t = torch.as_tensor(self.inverse_perm, device=self.device)
+        self._cache = None
+
+    def forward(self, x):
+        shape = tuple(x.shape) if hasattr(x, "shape") else np.shape(x)
+        if shape[1:] != (self.n_in,):
+            raise ValueError(f"PermutationLayer expects (batch, {self.n_in}) input")
+        x, host = self._check_input(x)
+        self._cache = True
+        return self._out(x.index_select(1, self._perm_t), host)
+
+    def backward(self, grad_y, retain_cache=False):
+        self._take_cache(retain_cache)
+        gy, host = self._check_input(grad_y)
+        return self._out(gy.index_select(1, self._inv_t), host)
+
+
+class DenseLayer(Layer):
+    """Dense y = xW + b baseline (layers.py:268-306), via cuBLAS (comparator only)."""
+
+    def __init__(self, n_in, n_out, rng=None, device=None):
+        self.n_in, self.n_out = n_in, n_out
+        self.device = _device(device)
+        kw = dict(dtype=torch.float32, device=self.device)
+        if rng is not None:
+            bound = np.sqrt(6.0 / (n_in + n_out))
+            self.w = torch.as_tensor(rng.uniform(n_in, n_out, -bound, bound), **kw)
+        else:
+            self.w = torch.zeros(n_in, n_out, **kw)
+        self.b = torch.zeros(n_out, **kw)
+        self.grad_w = torch.zeros(n_in, n_out, **kw)
+        self.grad_b = torch.zeros(n_out, **kw)
+        self._params = [Param("w", self.w, self.grad_w, decay=True), Param("b", self.b, self.grad_b)]
+        self._cache = None
+
+    def params(self):
+        return self._params
+
+    def param_count(self):
+        return self.n_in * self.n_out + self.n_out
+
+    def forward(self, x):
+        x, host = self._check_input(x)
+        self._cache = x
+        return self._out(torch.addmm(self.b, x, self.w), host)
+
+    def backward(self, grad_y, retain_cache=False):
+        x = self._take_cache(retain_cache)
+        if isinstance(grad_y, torch.Tensor) and grad_y.is_cuda:
+            gy, host = grad_y.to(torch.float32), False
+        else:
+            gy, host = torch.as_tensor(np.asarray(grad_y), dtype=torch.float32).to(self.device), True
+        if tuple(gy.shape) != (x.shape[0], self.n_out):
+            raise ValueError(f"gradient shape {tuple(gy.shape)} does not match output")
+        self.grad_w.addmm_(x.t(), gy)
+        self.grad_b.add_(gy.sum(0))
+        return self._out(gy @ self.w.t(), host)
+
+
+class Cascade:
+    """Ordered layer stack with a unified forward/backward contract (layers.py:309-357)."""
+
+    def __init__(self, layers):
+        layers = list(layers)
+        if not layers:
+            raise ValueError("cascade needs at least one layer")
+        for prev, nxt in zip(layers, layers[1:]):
+            if prev.n_out != nxt.n_in:
+                raise ValueError(
+                    f"adjacent sizes differ: {type(prev).__name__} outputs {prev.n_out}, "
+                    f"{type(nxt).__name__} expects {nxt.n_in}"
+                )
+        domains = {l.complex_domain for l in layers if not isinstance(l, PermutationLayer)}
+        if len(domains) > 1:
+            raise ValueError("cannot mix complex and real layers in one cascade")
+        self.layers = layers
+        self.complex_domain = any(l.complex_domain for l in layers)
+
+    @property
+    def n_in(self):
+        return self.layers[0].n_in
+
+    @property
+    def n_out(self):
+        return self.layers[-1].n_out
+
+    def forward(self, x):
+        host = not (isinstance(x, torch.Tensor) and x.is_cuda)
+        for layer in self.layers:
+            x = layer.forward(x if not isinstance(x, np.ndarray) else x)
+            if isinstance(x, np.ndarray):  # keep intermediates on device
+                x = torch.as_tensor(x, dtype=torch.float32, device=layer.device)
+        return Layer._out(x, host)
+
+    def backward(self, grad_y, retain_cache=False):
+        host = not (isinstance(grad_y, torch.Tensor) and grad_y.is_cuda)
+        g = grad_y
+        if host:
+            g = torch.as_tensor(np.asarray(grad_y), dtype=torch.float32).to(self.layers[-1].device)
+        for layer in reversed(self.layers):
+            g = layer.backward(g, retain_cache=retain_cache)
+        return Layer._out(g, host)
+
+    def params(self):
+        out = []
+        for layer in self.layers:
+            out.extend(layer.params())
+        return out
+
+    def param_count(self):
+        return sum(layer.param_count() for layer in self.layers)
+
+    def zero_grads(self):
+        for layer in self.layers:
+            layer.zero_grads()
+
+
+def acdc_cascade(n, depth, dct_mode="fast", backend="auto", device=None):
+    """``depth`` identity-configured ACDC layers of size n (layers.py:360-362)."""
+    return Cascade([AcdcLayer(n, dct_mode=dct_mode, backend=backend, device=device) for _ in range(depth)])
+
+
+def count_params(obj):
+    """3N per ACDC, 4N per AFDF, N*M+M per dense (layers.py:461-463)."""
+    return obj.param_count()

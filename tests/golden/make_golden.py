@@ -1,0 +1,142 @@
+"""Generate golden vectors by running the REFERENCE package itself.
+
+Run in the build container only (``/root/reference`` does not exist on the
+GPU box):  ``python tests/golden/make_golden.py``.  Writes
+``tests/golden/golden.npz``.
+
+The reference package (``/root/reference/pkg/src/acdc``) is imported in place
+(read-only).  Its compiled Cython backend is the one ``oracle/build_ref.py``
+builds from the reference's own ``_kernels.pyx``; it is injected as
+``acdc._kernels`` so ``backend.get_kernels("compiled")`` resolves to it
+(``backend.py:20-25,38-41``).  Every input is fp32-representable (drawn in fp32,
+then up-cast) so the same inputs feed the fp32 CUDA kernels in the GPU tests.
+
+Cases (keys prefixed per case):
+  dct_N*:   dct / idct of a (3, N) batch, N in {1,2,4,...,1024}   (transforms.py:137-156)
+  acdc_*:   AcdcLayer forward, backward twice (accumulation)        (layers.py:141-156)
+  afdf_*:   AfdfLayer forward/backward, complex                     (layers.py:199-215)
+  casc_*:   Cascade of ACDC / ReLU / Permutation                    (layers.py:336-344)
+  ka_*:     SPEC known answers (ones vector, identity layer, a = 0)
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+REF_SRC = "/root/reference/pkg/src"
+
+
+def import_reference():
+    from oracle import ref_kernels
+
+    mod = ref_kernels.load()
+    if mod is None:
+        raise SystemExit("oracle/_ref could not be built")
+    sys.modules["acdc._kernels"] = mod
+    sys.path.insert(0, REF_SRC)
+    import acdc  # noqa: E402  (the reference package)
+
+    assert acdc.backend.get_kernels("compiled") is mod
+    return acdc
+
+
+def f32(rng, *shape, mean=0.0, std=1.0):
+    return (mean + std * rng.standard_normal(shape)).astype(np.float32).astype(np.float64)
+
+
+def main():
+    acdc = import_reference()
+    rng = np.random.default_rng(20251017)
+    out = {}
+
+    for n in [1, 2, 4, 8, 16, 32, 64, 128, 256, 1024]:
+        plan = acdc.DctPlan(n, mode="fast", backend="compiled")
+        x = f32(rng, 3, n)
+        out[f"dct_N{n}_x"] = x
+        out[f"dct_N{n}_dct"] = acdc.dct(plan, x)
+        out[f"dct_N{n}_idct"] = acdc.idct(plan, x)
+
+    acdc_cases = [(2, 1), (4, 3), (8, 1), (16, 3), (32, 5), (64, 2), (128, 7), (256, 4), (1024, 3)]
+    for n, b in acdc_cases:
+        layer = acdc.AcdcLayer(n, dct_mode="fast", backend="compiled")
+        layer.a[:] = f32(rng, n, mean=1.0, std=0.4)   # gradcheck.py:98-100
+        layer.d[:] = f32(rng, n, mean=1.0, std=0.4)
+        layer.bias_d[:] = f32(rng, n, std=0.3)
+        x = f32(rng, b, n)
+        dy = f32(rng, b, n)
+        y = layer.forward(x)
+        dx = layer.backward(dy, retain_cache=True)
+        g1 = (layer.grad_a.copy(), layer.grad_d.copy(), layer.grad_bias_d.copy())
+        layer.backward(dy)  # accumulates (layers.py:152-155)
+        p = f"acdc_N{n}_B{b}_"
+        out[p + "a"], out[p + "d"], out[p + "bias"] = layer.a.copy(), layer.d.copy(), layer.bias_d.copy()
+        out[p + "x"], out[p + "dy"], out[p + "y"], out[p + "dx"] = x, dy, y, dx
+        out[p + "ga"], out[p + "gd"], out[p + "gb"] = g1
+        out[p + "ga2"], out[p + "gd2"], out[p + "gb2"] = layer.grad_a.copy(), layer.grad_d.copy(), layer.grad_bias_d.copy()
+
+    for n, b in [(4, 1), (16, 3), (64, 2), (256, 3), (1024, 2)]:
+        layer = acdc.AfdfLayer(n, backend="compiled")
+        layer.a[:] = f32(rng, n, mean=1.0, std=0.3) + 1j * f32(rng, n, std=0.3)  # gradcheck.py:105-106
+        layer.d[:] = f32(rng, n, mean=1.0, std=0.3) + 1j * f32(rng, n, std=0.3)
+        x = f32(rng, b, n) + 1j * f32(rng, b, n)
+        dy = f32(rng, b, n) + 1j * f32(rng, b, n)
+        y = layer.forward(x)
+        dx = layer.backward(dy)
+        p = f"afdf_N{n}_B{b}_"
+        out[p + "a"], out[p + "d"], out[p + "x"], out[p + "dy"] = layer.a.copy(), layer.d.copy(), x, dy
+        out[p + "y"], out[p + "dx"], out[p + "ga"], out[p + "gd"] = y, dx, layer.grad_a.copy(), layer.grad_d.copy()
+
+    # cascade: ACDC -> ReLU -> Perm repeated, no ReLU/Perm after the last ACDC
+    for n, depth, b in [(16, 3, 4), (64, 4, 3), (256, 3, 2)]:
+        prng = acdc.Rng(7 + n)
+        layers = []
+        for i in range(depth):
+            L = acdc.AcdcLayer(n, backend="compiled")
+            L.a[:] = f32(rng, n, mean=1.0, std=0.2)
+            L.d[:] = f32(rng, n, mean=1.0, std=0.2)
+            L.bias_d[:] = f32(rng, n, std=0.1)
+            layers.append(L)
+            if i < depth - 1:
+                layers.append(acdc.ReluLayer(n))
+                layers.append(acdc.PermutationLayer(n, rng=prng))
+        cas = acdc.Cascade(layers)
+        x = f32(rng, b, n)
+        dy = f32(rng, b, n)
+        y = cas.forward(x)
+        dx = cas.backward(dy)
+        p = f"casc_N{n}_K{depth}_B{b}_"
+        out[p + "x"], out[p + "dy"], out[p + "y"], out[p + "dx"] = x, dy, y, dx
+        li = 0
+        for L in layers:
+            if isinstance(L, acdc.AcdcLayer):
+                for nm in ("a", "d", "bias_d", "grad_a", "grad_d", "grad_bias_d"):
+                    out[p + f"L{li}_{nm}"] = getattr(L, nm).copy()
+                li += 1
+            elif isinstance(L, acdc.PermutationLayer):
+                out[p + f"P{li - 1}_perm"] = L.perm.copy()
+
+    # SPEC known answers
+    n = 16
+    plan = acdc.DctPlan(n, backend="compiled")
+    out["ka_dct_ones16"] = acdc.dct(plan, np.ones((1, n)))
+    ident = acdc.AcdcLayer(n, backend="compiled")
+    x = f32(rng, 2, n)
+    out["ka_ident_x"], out["ka_ident_y"] = x, ident.forward(x)
+    out["ka_ident_dx"] = ident.backward(x)
+    z = acdc.AcdcLayer(n, backend="compiled")
+    z.a[:] = 0.0
+    z.bias_d[:] = f32(rng, n)
+    out["ka_a0_bias"], out["ka_a0_y"] = z.bias_d.copy(), z.forward(x)
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
+    np.savez_compressed(path, **out)
+    print(f"wrote {path}: {len(out)} arrays, {os.path.getsize(path)} bytes")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,69 @@
+"""CPU tier: the C-ABI library loads and exports every symbol the header
+declares; argument validation that needs no GPU."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "acdc_b200.h")
+
+
+def _declared():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(acdc_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1511_05946_b200 import _lib, build
+
+    if not os.path.exists(_lib.LIB_PATH):
+        build.build()
+    return _lib.load()
+
+
+def test_header_symbols_exported(lib):
+    names = _declared()
+    assert "acdc_fwd_f32" in names and "acdc_bwd_f32" in names
+    for name in names:
+        assert hasattr(lib, name), f"{name} declared in acdc_b200.h but not exported"
+
+
+def test_binding_covers_header():
+    from paper_1511_05946_b200 import _lib
+
+    assert set(_declared()) == set(_lib.SIGNATURES)
+
+
+def test_abi_version_and_errors(lib):
+    from paper_1511_05946_b200 import _lib
+
+    assert lib.acdc_abi_version() == _lib.ABI_VERSION
+    assert lib.acdc_max_n() == 32768
+    # non-power-of-two n: the reference's ValueError message (transforms.py:96-97)
+    assert lib.acdc_prepare(12) == _lib.ACDC_E_SIZE
+    assert b"power-of-two" in lib.acdc_strerror(_lib.ACDC_E_SIZE)
+    with pytest.raises(ValueError, match="power-of-two size, got 12"):
+        _lib.check(lib.acdc_prepare(12))
+    assert lib.acdc_prepare(65536) == _lib.ACDC_E_SIZE
+    # shape validation happens before any device work
+    assert lib.acdc_fwd_f32(None, None, None, None, None, 4, 16, 8, 16, None) == _lib.ACDC_E_SHAPE
+    assert lib.acdc_fwd_f32(None, None, None, None, None, -1, 16, 16, 16, None) == _lib.ACDC_E_SHAPE
+    assert lib.acdc_fwd_f32(None, None, None, None, None, 4, 16, 16, 16, None) == _lib.ACDC_E_NULL
+    assert lib.acdc_dct2_f32(None, None, 3, 16, 16, 16, None) == _lib.ACDC_E_NULL
+    assert lib.acdc_bwd_workspace_bytes(16, 12) == 0
+    for code in (-2, -3, -4, -6):
+        assert lib.acdc_strerror(code)
+
+
+def test_no_cpu_fallback_in_product():
+    """The product package never imports the oracle."""
+    pkg = os.path.join(ROOT, "paper_1511_05946_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith(".py"):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|\"\"\"[\s\S]*?\"\"\"", "", src), f
