@@ -18,10 +18,17 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "../../include/acdc_b200.h"
 #include "dct_pair.cuh"
+
+#ifdef ACDC_NO_LB  // experiments: report the natural register demand
+#define ACDC_LB(G)
+#else
+#define ACDC_LB(G) __launch_bounds__(G::CTA, G::MINB)
+#endif
 
 namespace acdc {
 
@@ -32,29 +39,75 @@ struct KParams {
   const float* a;
   const float* d;
   const float* bias;
-  float* ws;  // bwd partials [groups][3][N]
-  const float2* tw;
-  const float2* cp;
+  float* ws;          // bwd partials [groups][3][N]
+  float* scratch;     // bwd stash when it does not fit in smem [groups][STASH*T]
+  const float2* tab;  // [pass twiddles | c'_k]
   int64_t rows;
   int64_t ldx, ldy, ldo;
 };
 
 // ---------------------------------------------------------------- helpers
 
+// Bulk prefetch of one row into L2 (TMA engine; no registers, no smem).
+__device__ __forceinline__ void prefetch_row_l2(const float* row, int n) {
+  uintptr_t a = reinterpret_cast<uintptr_t>(row);
+  uintptr_t lo = a & ~uintptr_t(15);
+  uintptr_t hi = (a + uintptr_t(n) * 4 + 15) & ~uintptr_t(15);
+  for (uintptr_t p = lo; p < hi; p += 32768) {
+    uint32_t bytes = (uint32_t)((hi - p) < 32768 ? (hi - p) : 32768);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+  }
+}
+
+// Plain (coherent) global load: unlike ld.global.nc it is ordered by the group
+// barriers, so ptxas cannot hoist it to the top of the row iteration where it
+// would pin a register across every FFT pass.
+__device__ __forceinline__ float ld_plain(const float* p) {
+  float r;
+  asm volatile("ld.global.f32 %0, [%1];" : "=f"(r) : "l"(p) : "memory");
+  return r;
+}
+
+// Row pointers of the Makhoul-reordered first/last pass slots of thread t.
+template <class G>
+struct RowPtr {
+  const float* lo;  // row + 2t
+  const float* hi;  // row + 2N-1-2t
+  __device__ __forceinline__ RowPtr(const float* row, int t) : lo(row + 2 * t), hi(row + (2 * G::N - 1 - 2 * t)) {}
+  template <int P>
+  __device__ __forceinline__ const float* at(int b, int q) const {
+    using M = RowMap<G, P>;
+    return M::lower(q) ? lo + M::off(b, q) : hi - M::off(b, q);
+  }
+};
+template <class G>
+struct RowPtrW {
+  float* lo;
+  float* hi;
+  __device__ __forceinline__ RowPtrW(float* row, int t) : lo(row + 2 * t), hi(row + (2 * G::N - 1 - 2 * t)) {}
+  template <int P>
+  __device__ __forceinline__ float* at(int b, int q) const {
+    using M = RowMap<G, P>;
+    return M::lower(q) ? lo + M::off(b, q) : hi - M::off(b, q);
+  }
+};
+
 // Load pass-0 inputs of the packed FFT: v = (xA * s, xB * s) at reorder_src(m).
 template <class G, bool SCALE>
-__device__ __forceinline__ void load_rows(float2 (&v)[G::E], const float* __restrict__ xa, const float* __restrict__ xb,
-                                          const float* __restrict__ s, int t) {
+__device__ __forceinline__ void load_rows(float2 (&v)[G::E], const float* xa, const float* xb, const float* s,
+                                          int t) {
   constexpr int R = G::radix(0);
+  const RowPtr<G> pa(xa, t);
+  const RowPtr<G> pb(xb ? xb : xa, t);
+  const RowPtr<G> ps(s ? s : xa, t);
 #pragma unroll
   for (int b = 0; b < G::E / R; ++b)
 #pragma unroll
     for (int q = 0; q < R; ++q) {
-      const int src = reorder_src<G::N>(first_pos<G>(t, b, q));
-      float va = __ldg(xa + src);
-      float vb = xb ? __ldg(xb + src) : 0.f;
+      float va = __ldg(pa.template at<0>(b, q));
+      float vb = xb ? __ldg(pb.template at<0>(b, q)) : 0.f;
       if constexpr (SCALE) {
-        const float sc = __ldg(s + src);
+        const float sc = __ldg(ps.template at<0>(b, q));
         va *= sc;
         vb *= sc;
       }
@@ -62,36 +115,26 @@ __device__ __forceinline__ void load_rows(float2 (&v)[G::E], const float* __rest
     }
 }
 
-// Forward DCT-II of the packed rows: on return X[2i], X[2i+1] hold bins lo/hi
-// of pair slot i as (rowA, rowB).
+// DCT-II post-pass over all slots (Z pairs -> bins, in place).
 template <class G>
-__device__ __forceinline__ void packed_dct2(float2 (&v)[G::E], float2 (&X)[G::E], Xbuf<G>& xb,
-                                            const GroupSync<G>& gs, const float2* __restrict__ tw,
-                                            const float2* __restrict__ cp, int t) {
-  fft_passes<G>(v, xb, gs, tw, t);
-  gather_pairs<G>(v, X, xb, gs, t);
-  const float2 chi = __ldg(cp + G::N / 2);
+__device__ __forceinline__ void post_all(float2 (&X)[G::E], const float2* cp, int t) {
+  const Slots<G> sl(t);
+  const float2 chi = tab_load<G>(cp, G::N / 2);
 #pragma unroll
-  for (int i = 0; i < G::E / 2; ++i) {
-    const int lo = t + i * G::T;
-    const float2 c = __ldg(cp + lo);
-    dct2_post<G>(X[2 * i], X[2 * i + 1], c, lo == 0, chi, X[2 * i], X[2 * i + 1]);
-  }
+  for (int i = 0; i < G::E / 2; ++i)
+    dct2_post(X[2 * i], X[2 * i + 1], tab_load<G>(sl.plo(cp, i), 0), sl.special(i), chi, X[2 * i], X[2 * i + 1]);
 }
 
-// DCT-III of packed bins Y (pair-slot layout); on return v holds
-// H[last_pos] with rowA = H.x, rowB = -H.y.
+// DCT-III pre-pass, exchange and FFT: Y (pair-slot bins) -> v = H[last_pos]
+// with rowA = H.x, rowB = -H.y.
 template <class G>
 __device__ __forceinline__ void packed_dct3(float2 (&Y)[G::E], float2 (&v)[G::E], Xbuf<G>& xb,
-                                            const GroupSync<G>& gs, const float2* __restrict__ tw,
-                                            const float2* __restrict__ cp, int t) {
-  const float2 chi = __ldg(cp + G::N / 2);
+                                            const GroupSync<G>& gs, const float2* tw, const float2* cp, int t) {
+  const Slots<G> sl(t);
+  const float2 chi = tab_load<G>(cp, G::N / 2);
 #pragma unroll
-  for (int i = 0; i < G::E / 2; ++i) {
-    const int lo = t + i * G::T;
-    const float2 c = __ldg(cp + lo);
-    dct3_pre<G>(Y[2 * i], Y[2 * i + 1], c, lo == 0, chi, Y[2 * i], Y[2 * i + 1]);
-  }
+  for (int i = 0; i < G::E / 2; ++i)
+    dct3_pre(Y[2 * i], Y[2 * i + 1], tab_load<G>(sl.plo(cp, i), 0), sl.special(i), chi, Y[2 * i], Y[2 * i + 1]);
   scatter_pairs_to_fft<G>(Y, v, xb, gs, t);
   fft_passes<G>(v, xb, gs, tw, t);
 }
@@ -112,43 +155,112 @@ __device__ __forceinline__ GroupCtx<G> group_ctx() {
   return c;
 }
 
+// Stage the pass-twiddle / post-twiddle tables in shared memory (whole CTA)
+// when the plan has room; return the table pointers the kernel should use.
+template <class G>
+__device__ __forceinline__ void stage_tables(const KParams& p, float* smem, const float2*& tw, const float2*& cp) {
+  constexpr int TOT = G::TW_ENTRIES + G::CP_ENTRIES;
+  if constexpr (G::TW_SMEM) {
+    float2* st = reinterpret_cast<float2*>(smem);
+    for (int i = threadIdx.x; i < TOT; i += blockDim.x) st[i] = p.tab[i];
+    __syncthreads();
+    tw = st;
+  } else {
+    tw = p.tab;
+  }
+  cp = tw + G::TW_ENTRIES;
+}
+
 // ---------------------------------------------------------------- kernels
 
 // y = C3(d * C2(a * x) + bias)          (layers.py:141-146)
 template <int LOGN>
-__global__ void __launch_bounds__(Geo<LOGN>::CTA, Geo<LOGN>::MINB) acdc_fwd_kernel(KParams p) {
+__global__ void ACDC_LB(Geo<LOGN>) acdc_fwd_kernel(KParams p) {
   using G = Geo<LOGN>;
+  constexpr int E = G::E;
+  constexpr int PL = G::NPASS - 1;
   extern __shared__ __align__(16) float smem_f[];
   const auto c = group_ctx<G>();
+  const int t = c.t;
   GroupSync<G> gs(c.grp);
-  Xbuf<G> xb{smem_f + c.grp * G::NBUF * G::BUF_FLOATS, 0};
+  Xbuf<G> xb{smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS, 0};
+  const float2 *tw, *cp;
+  stage_tables<G>(p, smem_f, tw, cp);
   const int64_t npairs = (p.rows + 1) >> 1;
+  if constexpr (G::FP) {
+    const FastMap<G> fm(t, gs.mask);
+    for (int64_t rp = c.gid; rp < npairs; rp += c.gstride) {
+      const int64_t ra = 2 * rp;
+      const bool hasb = ra + 1 < p.rows;
+      if (t == 0 && rp + c.gstride < npairs) {  // next row pair -> L2
+        const int64_t nr = 2 * (rp + c.gstride);
+        prefetch_row_l2(p.x + nr * p.ldx, G::N);
+        if (nr + 1 < p.rows) prefetch_row_l2(p.x + (nr + 1) * p.ldx, G::N);
+      }
+      float2 v[16];
+      fp_load<G, true>(v, p.x + ra * p.ldx, hasb ? p.x + (ra + 1) * p.ldx : nullptr, p.a, fm);
+      fft_passes<G, 0>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
+      {
+        float2 w[8], gl[8], gh[8];
+        fp_partner<G>(v, w, fm);
+        const float2 chi = tab_load<G>(cp, G::N / 2);
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const float2 cs = tab_load<G>(fm.plo(cp, s), 0);
+          float2 xl, xh;
+          dct2_post(v[s], w[s], cs, fm.special(s), chi, xl, xh);
+          const float dl = ld_plain(fm.plo(p.d, s)), bl = ld_plain(fm.plo(p.bias, s));
+          const float dh = ld_plain(fm.phi(p.d, s)), bh = ld_plain(fm.phi(p.bias, s));
+          xl = make_float2(fmaf(xl.x, dl, bl), fmaf(xl.y, dl, bl));
+          xh = make_float2(fmaf(xh.x, dh, bh), fmaf(xh.y, dh, bh));
+          dct3_pre(xl, xh, cs, fm.special(s), chi, gl[s], gh[s]);
+        }
+        fp_scatter<G>(gl, gh, v, fm);
+      }
+      fft_passes<G, 0>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
+      float2 oa[8], ob[8];
+      fp_out_pairs<G>(v, oa, ob, fm);
+      float2* ya = reinterpret_cast<float2*>(p.y + ra * p.ldo + 2 * fm.jsp);
+      float2* yb = reinterpret_cast<float2*>(p.y + (hasb ? ra + 1 : ra) * p.ldo + 2 * fm.jsp);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        ya[q * FastMap<G>::S] = oa[q];
+        if (hasb) yb[q * FastMap<G>::S] = ob[q];
+      }
+    }
+    return;
+  }
+  const Slots<G> sl(t);
   for (int64_t rp = c.gid; rp < npairs; rp += c.gstride) {
     const int64_t ra = 2 * rp;
     const bool hasb = ra + 1 < p.rows;
-    float2 v[G::E], X[G::E];
-    load_rows<G, true>(v, p.x + ra * p.ldx, hasb ? p.x + (ra + 1) * p.ldx : nullptr, p.a, c.t);
-    packed_dct2<G>(v, X, xb, gs, p.tw, p.cp, c.t);
+    if (t == 0 && rp + c.gstride < npairs) {  // next row pair -> L2
+      const int64_t nr = 2 * (rp + c.gstride);
+      prefetch_row_l2(p.x + nr * p.ldx, G::N);
+      if (nr + 1 < p.rows) prefetch_row_l2(p.x + (nr + 1) * p.ldx, G::N);
+    }
+    float2 v[E], X[E];
+    load_rows<G, true>(v, p.x + ra * p.ldx, hasb ? p.x + (ra + 1) * p.ldx : nullptr, p.a, t);
+    fft_passes<G>(v, xb, gs, tw, t);
+    gather_pairs<G>(v, X, xb, gs, t);
+    post_all<G>(X, cp, t);
 #pragma unroll
-    for (int i = 0; i < G::E / 2; ++i) {
-      int lo, hi;
-      slot_bins<G>(c.t, i, lo, hi);
-      const float dl = __ldg(p.d + lo), bl = __ldg(p.bias + lo);
-      const float dh = __ldg(p.d + hi), bh = __ldg(p.bias + hi);
+    for (int i = 0; i < E / 2; ++i) {
+      const float dl = ld_plain(sl.plo(p.d, i)), bl = ld_plain(sl.plo(p.bias, i));
+      const float dh = ld_plain(sl.phi(p.d, i)), bh = ld_plain(sl.phi(p.bias, i));
       X[2 * i] = make_float2(fmaf(X[2 * i].x, dl, bl), fmaf(X[2 * i].y, dl, bl));
       X[2 * i + 1] = make_float2(fmaf(X[2 * i + 1].x, dh, bh), fmaf(X[2 * i + 1].y, dh, bh));
     }
-    packed_dct3<G>(X, v, xb, gs, p.tw, p.cp, c.t);
-    float* ya = p.y + ra * p.ldo;
-    float* yb = p.y + (ra + 1) * p.ldo;
-    constexpr int RL = G::radix(G::NPASS - 1);
+    packed_dct3<G>(X, v, xb, gs, tw, cp, t);
+    constexpr int RL = G::radix(PL);
+    const RowPtrW<G> ya(p.y + ra * p.ldo, t);
+    const RowPtrW<G> yb(p.y + (hasb ? ra + 1 : ra) * p.ldo, t);
 #pragma unroll
-    for (int b = 0; b < G::E / RL; ++b)
+    for (int b = 0; b < E / RL; ++b)
 #pragma unroll
       for (int q = 0; q < RL; ++q) {
-        const int dst = reorder_src<G::N>(last_pos<G>(c.t, b, q));
-        ya[dst] = v[b * RL + q].x;
-        if (hasb) yb[dst] = -v[b * RL + q].y;
+        *ya.template at<PL>(b, q) = v[b * RL + q].x;
+        if (hasb) *yb.template at<PL>(b, q) = -v[b * RL + q].y;
       }
   }
 }
@@ -156,20 +268,39 @@ __global__ void __launch_bounds__(Geo<LOGN>::CTA, Geo<LOGN>::MINB) acdc_fwd_kern
 // Backward (layers.py:148-156) with h2 recomputed:
 //   g3 = C2(dy); h2 = C2(a*x); gb += sum g3; gd += sum h2*g3;
 //   g1 = C3(d*g3); ga += sum x*g1; dx = a*g1.
-// Parameter-gradient partials stay in registers (each thread owns fixed bins
-// and positions across all its rows) and are written once per group to ws.
+// Each thread owns fixed bins / positions across all its rows: grad_bias and
+// grad_d partials stay in registers, grad_a partials and g3 live in a
+// thread-private shared-memory stash (layout [slot][t], conflict-free).  The
+// partials are written once per group to ws and reduced by
+// acdc_grad_reduce_kernel.
 template <int LOGN>
-__global__ void __launch_bounds__(Geo<LOGN>::CTA, Geo<LOGN>::MINB) acdc_bwd_kernel(KParams p) {
-  using G = Geo<LOGN>;
+using GeoBwd = Geo<LOGN, 3 * Geo<LOGN>::E>;  // stash: g3 (E float2) + grad_a (E floats)
+
+template <int LOGN>
+__global__ void ACDC_LB(GeoBwd<LOGN>) acdc_bwd_kernel(KParams p) {
+  using G = GeoBwd<LOGN>;
   constexpr int E = G::E;
-  constexpr int RL = G::radix(G::NPASS - 1);
+  constexpr int T = G::T;
+  constexpr int PL = G::NPASS - 1;
+  constexpr int RL = G::radix(PL);
   extern __shared__ __align__(16) float smem_f[];
   const auto c = group_ctx<G>();
+  const int t = c.t;
   GroupSync<G> gs(c.grp);
-  Xbuf<G> xb{smem_f + c.grp * G::NBUF * G::BUF_FLOATS, 0};
-  float acc_a[E], acc_d[E], acc_b[E];
+  float* gbase = smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS;
+  Xbuf<G> xb{gbase, 0};
+  float* sbase = G::STASH_SMEM ? gbase + G::NBUF * G::BUF_FLOATS : p.scratch + c.gid * G::GSCRATCH_FLOATS;
+  float2* st_g3 = reinterpret_cast<float2*>(sbase) + t;  // [E][T]
+  float* st_ga = sbase + 2 * E * T + t;                  // [E][T]
+  const float2 *tw, *cp;
+  stage_tables<G>(p, smem_f, tw, cp);
+  const Slots<G> sl(t);
+  float acc_d[E], acc_b[E];
 #pragma unroll
-  for (int i = 0; i < E; ++i) acc_a[i] = acc_d[i] = acc_b[i] = 0.f;
+  for (int i = 0; i < E; ++i) {
+    acc_d[i] = acc_b[i] = 0.f;
+    st_ga[i * T] = 0.f;
+  }
 
   const int64_t npairs = (p.rows + 1) >> 1;
   for (int64_t rp = c.gid; rp < npairs; rp += c.gstride) {
@@ -177,129 +308,154 @@ __global__ void __launch_bounds__(Geo<LOGN>::CTA, Geo<LOGN>::MINB) acdc_bwd_kern
     const bool hasb = ra + 1 < p.rows;
     const float* xa = p.x + ra * p.ldx;
     const float* xbp = hasb ? p.x + (ra + 1) * p.ldx : nullptr;
-    float2 v[E], g3[E];
-    // g3 = C2(dy)
-    load_rows<G, false>(v, p.dy + ra * p.ldy, hasb ? p.dy + (ra + 1) * p.ldy : nullptr, nullptr, c.t);
-    packed_dct2<G>(v, g3, xb, gs, p.tw, p.cp, c.t);
-    // h2 = C2(a*x), consumed slot by slot
+    if (t == 0 && rp + c.gstride < npairs) {  // next row pair -> L2
+      const int64_t nr = 2 * (rp + c.gstride);
+      prefetch_row_l2(p.dy + nr * p.ldy, G::N);
+      prefetch_row_l2(p.x + nr * p.ldx, G::N);
+      if (nr + 1 < p.rows) {
+        prefetch_row_l2(p.dy + (nr + 1) * p.ldy, G::N);
+        prefetch_row_l2(p.x + (nr + 1) * p.ldx, G::N);
+      }
+    }
+    float2 v[E];
+    // g3 = C2(dy): grad_bias partial, then stash
     {
-      float2 h2[E];
-      load_rows<G, true>(v, xa, xbp, p.a, c.t);
-      packed_dct2<G>(v, h2, xb, gs, p.tw, p.cp, c.t);
+      float2 g3[E];
+      load_rows<G, false>(v, p.dy + ra * p.ldy, hasb ? p.dy + (ra + 1) * p.ldy : nullptr, nullptr, t);
+      fft_passes<G>(v, xb, gs, tw, t);
+      gather_pairs<G>(v, g3, xb, gs, t);
+      post_all<G>(g3, cp, t);
 #pragma unroll
       for (int i = 0; i < E; ++i) {
         acc_b[i] += g3[i].x + g3[i].y;
-        acc_d[i] = fmaf(h2[i].x, g3[i].x, fmaf(h2[i].y, g3[i].y, acc_d[i]));
+        st_g3[i * T] = g3[i];
       }
     }
-    // Y = d * g3
+    // h2 = C2(a*x) slot by slot: grad_d partial; Y = d * g3 for the inverse
+    float2 Y[E];
+    {
+      float2 zp[E];
+      load_rows<G, true>(v, xa, xbp, p.a, t);
+      fft_passes<G>(v, xb, gs, tw, t);
+      gather_pairs<G>(v, zp, xb, gs, t);
+      const float2 chi = tab_load<G>(cp, G::N / 2);
 #pragma unroll
-    for (int i = 0; i < E / 2; ++i) {
-      int lo, hi;
-      slot_bins<G>(c.t, i, lo, hi);
-      const float dl = __ldg(p.d + lo), dh = __ldg(p.d + hi);
-      g3[2 * i] = make_float2(g3[2 * i].x * dl, g3[2 * i].y * dl);
-      g3[2 * i + 1] = make_float2(g3[2 * i + 1].x * dh, g3[2 * i + 1].y * dh);
+      for (int i = 0; i < E / 2; ++i) {
+        float2 hl, hh;
+        dct2_post(zp[2 * i], zp[2 * i + 1], tab_load<G>(sl.plo(cp, i), 0), sl.special(i), chi, hl, hh);
+        const float2 gl = st_g3[(2 * i) * T], gh = st_g3[(2 * i + 1) * T];
+        acc_d[2 * i] = fmaf(hl.x, gl.x, fmaf(hl.y, gl.y, acc_d[2 * i]));
+        acc_d[2 * i + 1] = fmaf(hh.x, gh.x, fmaf(hh.y, gh.y, acc_d[2 * i + 1]));
+        const float dl = ld_plain(sl.plo(p.d, i)), dh = ld_plain(sl.phi(p.d, i));
+        Y[2 * i] = make_float2(gl.x * dl, gl.y * dl);
+        Y[2 * i + 1] = make_float2(gh.x * dh, gh.y * dh);
+      }
     }
-    packed_dct3<G>(g3, v, xb, gs, p.tw, p.cp, c.t);
-    float* oa = p.y + ra * p.ldo;
-    float* ob = p.y + (ra + 1) * p.ldo;
+    // g1 = C3(Y); dx = a * g1; grad_a partial += x * g1
+    packed_dct3<G>(Y, v, xb, gs, tw, cp, t);
+    const RowPtrW<G> oa(p.y + ra * p.ldo, t);
+    const RowPtrW<G> ob(p.y + (hasb ? ra + 1 : ra) * p.ldo, t);
+    const RowPtr<G> pxa(xa, t), pxb(hasb ? xbp : xa, t), pa(p.a, t);
 #pragma unroll
     for (int b = 0; b < E / RL; ++b)
 #pragma unroll
       for (int q = 0; q < RL; ++q) {
-        const int dst = reorder_src<G::N>(last_pos<G>(c.t, b, q));
         const float g1a = v[b * RL + q].x, g1b = -v[b * RL + q].y;
-        const float av = __ldg(p.a + dst);
-        float s = g1a * __ldg(xa + dst);
-        oa[dst] = av * g1a;
+        const float av = ld_plain(pa.template at<PL>(b, q));
+        float s = g1a * ld_plain(pxa.template at<PL>(b, q));
+        *oa.template at<PL>(b, q) = av * g1a;
         if (hasb) {
-          s = fmaf(g1b, __ldg(xbp + dst), s);
-          ob[dst] = av * g1b;
+          s = fmaf(g1b, ld_plain(pxb.template at<PL>(b, q)), s);
+          *ob.template at<PL>(b, q) = av * g1b;
         }
-        acc_a[b * RL + q] += s;
+        st_ga[(b * RL + q) * T] += s;
       }
   }
   // per-group partials: ws[gid][0] = grad_a, [1] = grad_d, [2] = grad_bias
   float* w = p.ws + c.gid * 3 * G::N;
+  const RowPtrW<G> wa(w, t);
 #pragma unroll
   for (int b = 0; b < E / RL; ++b)
 #pragma unroll
-    for (int q = 0; q < RL; ++q) w[reorder_src<G::N>(last_pos<G>(c.t, b, q))] = acc_a[b * RL + q];
+    for (int q = 0; q < RL; ++q) *wa.template at<PL>(b, q) = st_ga[(b * RL + q) * T];
 #pragma unroll
   for (int i = 0; i < E / 2; ++i) {
-    int lo, hi;
-    slot_bins<G>(c.t, i, lo, hi);
-    w[G::N + lo] = acc_d[2 * i];
-    w[G::N + hi] = acc_d[2 * i + 1];
-    w[2 * G::N + lo] = acc_b[2 * i];
-    w[2 * G::N + hi] = acc_b[2 * i + 1];
+    *sl.plo(w + G::N, i) = acc_d[2 * i];
+    *sl.phi(w + G::N, i) = acc_d[2 * i + 1];
+    *sl.plo(w + 2 * G::N, i) = acc_b[2 * i];
+    *sl.phi(w + 2 * G::N, i) = acc_b[2 * i + 1];
   }
 }
 
 // Row-wise orthonormal DCT-II (transforms.py:137-145) / DCT-III (148-156).
 template <int LOGN>
-__global__ void __launch_bounds__(Geo<LOGN>::CTA, Geo<LOGN>::MINB) acdc_dct2_kernel(KParams p) {
+__global__ void ACDC_LB(Geo<LOGN>) acdc_dct2_kernel(KParams p) {
   using G = Geo<LOGN>;
   extern __shared__ __align__(16) float smem_f[];
   const auto c = group_ctx<G>();
+  const int t = c.t;
   GroupSync<G> gs(c.grp);
-  Xbuf<G> xb{smem_f + c.grp * G::NBUF * G::BUF_FLOATS, 0};
+  Xbuf<G> xb{smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS, 0};
+  const float2 *tw, *cp;
+  stage_tables<G>(p, smem_f, tw, cp);
+  const Slots<G> sl(t);
   const int64_t npairs = (p.rows + 1) >> 1;
   for (int64_t rp = c.gid; rp < npairs; rp += c.gstride) {
     const int64_t ra = 2 * rp;
     const bool hasb = ra + 1 < p.rows;
     float2 v[G::E], X[G::E];
-    load_rows<G, false>(v, p.x + ra * p.ldx, hasb ? p.x + (ra + 1) * p.ldx : nullptr, nullptr, c.t);
-    packed_dct2<G>(v, X, xb, gs, p.tw, p.cp, c.t);
+    load_rows<G, false>(v, p.x + ra * p.ldx, hasb ? p.x + (ra + 1) * p.ldx : nullptr, nullptr, t);
+    fft_passes<G>(v, xb, gs, tw, t);
+    gather_pairs<G>(v, X, xb, gs, t);
+    post_all<G>(X, cp, t);
     float* ya = p.y + ra * p.ldo;
-    float* yb = p.y + (ra + 1) * p.ldo;
+    float* yb = p.y + (hasb ? ra + 1 : ra) * p.ldo;
 #pragma unroll
     for (int i = 0; i < G::E / 2; ++i) {
-      int lo, hi;
-      slot_bins<G>(c.t, i, lo, hi);
-      ya[lo] = X[2 * i].x;
-      ya[hi] = X[2 * i + 1].x;
+      *sl.plo(ya, i) = X[2 * i].x;
+      *sl.phi(ya, i) = X[2 * i + 1].x;
       if (hasb) {
-        yb[lo] = X[2 * i].y;
-        yb[hi] = X[2 * i + 1].y;
+        *sl.plo(yb, i) = X[2 * i].y;
+        *sl.phi(yb, i) = X[2 * i + 1].y;
       }
     }
   }
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(Geo<LOGN>::CTA, Geo<LOGN>::MINB) acdc_dct3_kernel(KParams p) {
+__global__ void ACDC_LB(Geo<LOGN>) acdc_dct3_kernel(KParams p) {
   using G = Geo<LOGN>;
+  constexpr int PL = G::NPASS - 1;
   extern __shared__ __align__(16) float smem_f[];
   const auto c = group_ctx<G>();
+  const int t = c.t;
   GroupSync<G> gs(c.grp);
-  Xbuf<G> xb{smem_f + c.grp * G::NBUF * G::BUF_FLOATS, 0};
+  Xbuf<G> xb{smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS, 0};
+  const float2 *tw, *cp;
+  stage_tables<G>(p, smem_f, tw, cp);
+  const Slots<G> sl(t);
   const int64_t npairs = (p.rows + 1) >> 1;
   for (int64_t rp = c.gid; rp < npairs; rp += c.gstride) {
     const int64_t ra = 2 * rp;
     const bool hasb = ra + 1 < p.rows;
     const float* ya = p.x + ra * p.ldx;
-    const float* yb = p.x + (ra + 1) * p.ldx;
+    const float* yb = p.x + (hasb ? ra + 1 : ra) * p.ldx;
     float2 v[G::E], Y[G::E];
 #pragma unroll
     for (int i = 0; i < G::E / 2; ++i) {
-      int lo, hi;
-      slot_bins<G>(c.t, i, lo, hi);
-      Y[2 * i] = make_float2(__ldg(ya + lo), hasb ? __ldg(yb + lo) : 0.f);
-      Y[2 * i + 1] = make_float2(__ldg(ya + hi), hasb ? __ldg(yb + hi) : 0.f);
+      Y[2 * i] = make_float2(__ldg(sl.plo(ya, i)), hasb ? __ldg(sl.plo(yb, i)) : 0.f);
+      Y[2 * i + 1] = make_float2(__ldg(sl.phi(ya, i)), hasb ? __ldg(sl.phi(yb, i)) : 0.f);
     }
-    packed_dct3<G>(Y, v, xb, gs, p.tw, p.cp, c.t);
-    float* oa = p.y + ra * p.ldo;
-    float* ob = p.y + (ra + 1) * p.ldo;
-    constexpr int RL = G::radix(G::NPASS - 1);
+    packed_dct3<G>(Y, v, xb, gs, tw, cp, t);
+    constexpr int RL = G::radix(PL);
+    const RowPtrW<G> oa(p.y + ra * p.ldo, t);
+    const RowPtrW<G> ob(p.y + (hasb ? ra + 1 : ra) * p.ldo, t);
 #pragma unroll
     for (int b = 0; b < G::E / RL; ++b)
 #pragma unroll
       for (int q = 0; q < RL; ++q) {
-        const int dst = reorder_src<G::N>(last_pos<G>(c.t, b, q));
-        oa[dst] = v[b * RL + q].x;
-        if (hasb) ob[dst] = -v[b * RL + q].y;
+        *oa.template at<PL>(b, q) = v[b * RL + q].x;
+        if (hasb) *ob.template at<PL>(b, q) = -v[b * RL + q].y;
       }
   }
 }
@@ -333,27 +489,49 @@ __global__ void acdc_n1_bwd_kernel(KParams p) {
   if (threadIdx.x < 3) p.ws[threadIdx.x] = (float)red[threadIdx.x][0];
 }
 
-// grad_c[i] (+)= sum_g ws[g][c][i], summed in double in fixed group order.
-__global__ void acdc_grad_reduce_kernel(const float* __restrict__ ws, int64_t groups, int n, float* ga, float* gd,
-                                        float* gb, int accumulate) {
+// grad_c[i] (+)= sum_g ws[g][c][i] in double, in a fixed order: block b owns
+// 32 consecutive outputs; warp s sums groups s, s+8, s+16, ... and the 8 warp
+// partials are added in warp order.  Deterministic for a fixed group count.
+__global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __restrict__ ws, int64_t groups, int n,
+                                                               float* ga, float* gd, float* gb, int accumulate) {
+  __shared__ double part[8][33];
+  const int o = threadIdx.x & 31, s = threadIdx.x >> 5;
   const int64_t total = 3LL * n;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int comp = (int)(idx / n);
-    const int i = (int)(idx - (int64_t)comp * n);
-    double s = 0.0;
-    for (int64_t g = 0; g < groups; ++g) s += (double)ws[(g * 3 + comp) * n + i];
+  const int64_t idx = blockIdx.x * 32LL + o;
+  double acc = 0.0;
+  int comp = 0, i = 0;
+  if (idx < total) {
+    comp = (int)(idx / n);
+    i = (int)(idx - (int64_t)comp * n);
+    const float* base = ws + (int64_t)comp * n + i;
+    const int64_t gstride = 3LL * n;
+    int64_t g = s;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (; g + 24 < groups; g += 32) {
+      a0 += (double)base[g * gstride];
+      a1 += (double)base[(g + 8) * gstride];
+      a2 += (double)base[(g + 16) * gstride];
+      a3 += (double)base[(g + 24) * gstride];
+    }
+    for (; g < groups; g += 8) a0 += (double)base[g * gstride];
+    acc = (a0 + a1) + (a2 + a3);
+  }
+  part[s][o] = acc;
+  __syncthreads();
+  if (s == 0 && idx < total) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += part[k][o];
     float* out = comp == 0 ? ga : (comp == 1 ? gd : gb);
-    if (accumulate) s += (double)out[i];
-    out[i] = (float)s;
+    if (accumulate) t += (double)out[i];
+    out[i] = (float)t;
   }
 }
 
 // ---------------------------------------------------------------- host side
 
 struct Tables {
-  float2* tw = nullptr;  // exp(-2 pi i t / N), t < N
-  float2* cp = nullptr;  // s_k exp(-i pi k / 2N) / 2, k <= N/2
+  float2* tab = nullptr;  // [pass twiddles W_{Ns R}^{q k} | c'_k = s_k e^{-i pi k/2N}/2, k <= N/2]
 };
 
 static std::mutex g_mu;
@@ -365,6 +543,27 @@ static int set_cuda_error(cudaError_t e) {
   snprintf(g_errbuf, sizeof(g_errbuf), "CUDA error: %s", cudaGetErrorString(e));
   g_last_error = g_errbuf;
   return ACDC_E_CUDA;
+}
+
+// exp(-2 pi i m / M) in double, rounded once to fp32
+static float2 twiddle(long m, long M) {
+  const double pi = 3.14159265358979323846264338327950288;
+  m %= M;
+  const double th = 2.0 * pi * (double)m / (double)M;
+  return make_float2((float)std::cos(th), (float)-std::sin(th));
+}
+
+// Host mirror of Plan<LOGN> (radix 16 x small x 16 ...).
+static void host_plan(int logn, std::vector<int>& radix) {
+  radix.clear();
+  const int n = 1 << logn;
+  if (logn < 4) {
+    radix.push_back(n);
+    return;
+  }
+  const int a16 = logn / 4, rem = logn % 4;
+  const int np = a16 + (rem ? 1 : 0);
+  for (int p = 0; p < np; ++p) radix.push_back((rem && p == 1) ? (1 << rem) : 16);
 }
 
 static int get_tables(int logn, Tables* out) {
@@ -379,23 +578,25 @@ static int get_tables(int logn, Tables* out) {
     return ACDC_OK;
   }
   const int n = 1 << logn;
-  std::vector<float2> tw(n), cp(n / 2 + 1);
-  const double pi = 3.14159265358979323846264338327950288;
-  for (int t = 0; t < n; ++t) {
-    const double th = 2.0 * pi * (double)t / (double)n;
-    tw[t] = make_float2((float)std::cos(th), (float)-std::sin(th));
+  std::vector<int> radix;
+  host_plan(logn, radix);
+  std::vector<float2> h;
+  long ns = radix[0];
+  for (size_t p = 1; p < radix.size(); ++p) {
+    const int r = radix[p];
+    for (int q = 1; q < r; ++q)
+      for (long k = 0; k < ns; ++k) h.push_back(twiddle((long)q * k, ns * r));
+    ns *= r;
   }
+  const double pi = 3.14159265358979323846264338327950288;
   for (int k = 0; k <= n / 2; ++k) {
     const double s = (k == 0 ? std::sqrt(1.0 / n) : std::sqrt(2.0 / n)) * 0.5;
     const double th = pi * (double)k / (2.0 * n);
-    cp[k] = make_float2((float)(s * std::cos(th)), (float)(-s * std::sin(th)));
+    h.push_back(make_float2((float)(s * std::cos(th)), (float)(-s * std::sin(th))));
   }
   Tables tb;
-  if ((e = cudaMalloc(&tb.tw, sizeof(float2) * n)) != cudaSuccess) return set_cuda_error(e);
-  if ((e = cudaMalloc(&tb.cp, sizeof(float2) * (n / 2 + 1))) != cudaSuccess) return set_cuda_error(e);
-  if ((e = cudaMemcpy(tb.tw, tw.data(), sizeof(float2) * n, cudaMemcpyHostToDevice)) != cudaSuccess)
-    return set_cuda_error(e);
-  if ((e = cudaMemcpy(tb.cp, cp.data(), sizeof(float2) * (n / 2 + 1), cudaMemcpyHostToDevice)) != cudaSuccess)
+  if ((e = cudaMalloc(&tb.tab, sizeof(float2) * h.size())) != cudaSuccess) return set_cuda_error(e);
+  if ((e = cudaMemcpy(tb.tab, h.data(), sizeof(float2) * h.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
     return set_cuda_error(e);
   g_tables[key] = tb;
   *out = tb;
@@ -408,17 +609,19 @@ struct LaunchInfo {
   const void* fn;
   int cta;
   int gpc;
+  int scratch;  // global scratch floats per group (bwd)
   int smem;
 };
 
 template <int LOGN>
 static LaunchInfo info_for(int kind) {
   using G = Geo<LOGN>;
+  using GB = GeoBwd<LOGN>;
   const void* fn = kind == K_FWD    ? (const void*)acdc_fwd_kernel<LOGN>
                    : kind == K_BWD  ? (const void*)acdc_bwd_kernel<LOGN>
                    : kind == K_DCT2 ? (const void*)acdc_dct2_kernel<LOGN>
                                     : (const void*)acdc_dct3_kernel<LOGN>;
-  return LaunchInfo{fn, G::CTA, G::GPC, G::SMEM_BYTES};
+  return LaunchInfo{fn, G::CTA, G::GPC, kind == K_BWD ? GB::GSCRATCH_FLOATS : 0, kind == K_BWD ? GB::SMEM_BYTES : G::SMEM_BYTES};
 }
 
 static int launch_info(int logn, int kind, LaunchInfo* li) {
@@ -427,6 +630,7 @@ static int launch_info(int logn, int kind, LaunchInfo* li) {
   case L:            \
     *li = info_for<L>(kind); \
     return ACDC_OK;
+#ifndef ACDC_ONLY_LOGN  // experiments: build a single size
     ACDC_CASE(1)
     ACDC_CASE(2)
     ACDC_CASE(3)
@@ -442,6 +646,9 @@ static int launch_info(int logn, int kind, LaunchInfo* li) {
     ACDC_CASE(13)
     ACDC_CASE(14)
     ACDC_CASE(15)
+#else
+    ACDC_CASE(ACDC_ONLY_LOGN)
+#endif
 #undef ACDC_CASE
     default:
       return ACDC_E_SIZE;
@@ -516,8 +723,7 @@ static int run(int kind, KParams p, int32_t n, cudaStream_t st) {
   if (p.rows == 0) return ACDC_OK;
   Tables tb;
   if ((rc = get_tables(logn, &tb))) return rc;
-  p.tw = tb.tw;
-  p.cp = tb.cp;
+  p.tab = tb.tab;
   LaunchInfo li;
   int64_t grid;
   if ((rc = grid_for(logn, kind, p.rows, &li, &grid))) return rc;
@@ -614,7 +820,7 @@ size_t acdc_bwd_workspace_bytes(int64_t rows, int32_t n) {
   LaunchInfo li;
   int64_t grid;
   if (grid_for(logn, K_BWD, rows > 0 ? rows : 1, &li, &grid)) return 0;
-  return (size_t)grid * li.gpc * 3 * (size_t)n * sizeof(float);
+  return (size_t)grid * li.gpc * (3 * (size_t)n + (size_t)li.scratch) * sizeof(float);
 }
 
 int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, const float* d, float* grad_a,
@@ -642,6 +848,12 @@ int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, con
   p.ldy = ldy;
   p.ldo = lddx;
   int64_t groups = 1;
+  if (n > 1) {  // scratch follows the partials
+    LaunchInfo li;
+    int64_t grid;
+    if ((rc = grid_for(logn, K_BWD, rows > 0 ? rows : 1, &li, &grid))) return rc;
+    p.scratch = p.ws + grid * li.gpc * 3 * (int64_t)n;
+  }
   if (rows == 0) {
     if (!accumulate) {
       cudaMemsetAsync(grad_a, 0, sizeof(float) * n, st);
@@ -661,7 +873,7 @@ int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, con
     groups = grid * li.gpc;
   }
   const int64_t total = 3LL * n;
-  int blocks = (int)((total + 255) / 256);
+  int blocks = (int)((total + 31) / 32);
   acdc_grad_reduce_kernel<<<blocks, 256, 0, st>>>((const float*)ws, groups, n, grad_a, grad_d, grad_bias,
                                                   accumulate);
   cudaError_t e = cudaGetLastError();

@@ -26,11 +26,36 @@
 
 namespace acdc {
 
+// Pair-slot addressing: bins lo = t + i*T and hi = N - lo.  Element pointers
+// for the hi bins are (base + N - t) - i*T; padded exchange indices are
+// padi(t) + padoff(iT) and padoff(N - iT) - hb(t) (T a multiple of 16).
 template <class G>
-__device__ __forceinline__ void slot_bins(int t, int i, int& lo, int& hi) {
-  lo = t + i * G::T;
-  hi = (lo == 0) ? (G::N / 2) : (G::N - lo);
-}
+struct Slots {
+  static constexpr int N = G::N, T = G::T, NS = G::E / 2;
+  int t;
+  bool t0;
+  __device__ __forceinline__ explicit Slots(int t_) : t(t_), t0(t_ == 0) {}
+  __device__ __forceinline__ bool special(int i) const { return i == 0 && t0; }
+  __device__ __forceinline__ int lo(int i) const { return t + i * T; }
+  __device__ __forceinline__ int hi(int i) const { return special(i) ? N / 2 : N - t - i * T; }
+  // element of an array indexed by bin: a[lo], a[hi]
+  template <class P>
+  __device__ __forceinline__ P* plo(P* a, int i) const { return a + t + i * T; }
+  template <class P>
+  __device__ __forceinline__ P* phi(P* a, int i) const {
+    return (i == 0) ? (t0 ? a + N / 2 : a + (N - t)) : (a + (N - t)) - i * T;
+  }
+  // padded exchange indices
+  __device__ __forceinline__ int xlo(int i) const { return padi(t) + padoff(i * T); }
+  __device__ __forceinline__ int xhi(int i) const {
+    if constexpr (T % 16 == 0) {
+      const int hb = t + ((t + 15) >> 4);
+      return (i == 0 && t0) ? padoff(N / 2) : padoff(N - i * T) - hb;
+    } else {
+      return padi(hi(i));
+    }
+  }
+};
 
 // Store the last-pass outputs (natural order) through an exchange, read back
 // the pair slots: zp[2i] = Z[lo_i], zp[2i+1] = Z[hi_i].
@@ -40,28 +65,27 @@ __device__ __forceinline__ void gather_pairs(const float2 (&v)[G::E], float2 (&z
   constexpr int P = G::NPASS - 1;
   constexpr int R = G::radix(P);
   constexpr int NB = G::E / R;
-  constexpr int STRIDE = G::N / R;
+  constexpr int S = G::N / R;
+  const Slots<G> sl(t);
   xchg(
       xb, gs,
       [&](const auto& put) {
+        const int pt = padi(t);
 #pragma unroll
         for (int b = 0; b < NB; ++b)
 #pragma unroll
-          for (int q = 0; q < R; ++q) put(t + b * G::T + q * STRIDE, v[b * R + q]);
+          for (int q = 0; q < R; ++q) put(pt + padoff(b * G::T) + padoff(q * S), v[b * R + q]);
       },
       [&](const auto& get) {
 #pragma unroll
         for (int i = 0; i < G::E / 2; ++i) {
-          int lo, hi;
-          slot_bins<G>(t, i, lo, hi);
-          get(lo, zp[2 * i]);
-          get(hi & (G::N - 1), zp[2 * i + 1]);
+          get(sl.xlo(i), zp[2 * i]);
+          get(sl.xhi(i), zp[2 * i + 1]);
         }
       });
 }
 
 // DCT-II post-pass for one slot: (Z[lo], Z[hi]) -> X[lo] = (XA, XB), X[hi].
-template <class G>
 __device__ __forceinline__ void dct2_post(float2 zlo, float2 zhi, float2 c, bool special, float2 c_hi, float2& xlo,
                                           float2& xhi) {
   if (special) {
@@ -80,7 +104,6 @@ __device__ __forceinline__ void dct2_post(float2 zlo, float2 zhi, float2 c, bool
 }
 
 // DCT-III pre-pass for one slot: Y[lo] = (YA, YB), Y[hi] -> G[lo], G[hi].
-template <class G>
 __device__ __forceinline__ void dct3_pre(float2 ylo, float2 yhi, float2 c, bool special, float2 c_hi, float2& glo,
                                          float2& ghi) {
   if (special) {
@@ -100,18 +123,129 @@ __device__ __forceinline__ void dct3_pre(float2 ylo, float2 yhi, float2 c, bool 
 template <class G>
 __device__ __forceinline__ void scatter_pairs_to_fft(const float2 (&gp)[G::E], float2 (&v)[G::E], Xbuf<G>& xb,
                                                      const GroupSync<G>& gs, int t) {
+  const Slots<G> sl(t);
   xchg(
       xb, gs,
       [&](const auto& put) {
 #pragma unroll
         for (int i = 0; i < G::E / 2; ++i) {
-          int lo, hi;
-          slot_bins<G>(t, i, lo, hi);
-          put(lo, gp[2 * i]);
-          if (hi != G::N) put(hi, gp[2 * i + 1]);
+          put(sl.xlo(i), gp[2 * i]);
+          put(sl.xhi(i), gp[2 * i + 1]);
         }
       },
       [&](const auto& get) { pass_load<G, 0>(v, get, t); });
+}
+
+// =====================================================================
+// Fast-pairing path (N >= 256, E = 16): the first and last pass have one
+// radix-16 butterfly per thread (T = S = N/16).  Butterflies are remapped so
+// that the two pairings the DCT needs sit in partner lanes (lane ^ H):
+//   spatial  j <-> S-1-j : x[2m], x[2m+1] are z[m] and z[N-1-m]  (Makhoul)
+//   frequency j <-> S-j  : Z[k] and Z[N-k]                       (real FFT)
+// so the pair exchanges are register shuffles, the DCT-II post-pass feeds
+// the DCT-III pre-pass without touching shared memory, and global rows are
+// moved as 64-bit pairs.  Butterflies 0 and S/2 are self-paired.
+template <class G>
+struct FastMap {
+  static constexpr int N = G::N;
+  static constexpr int S = G::N / 16;      // == T
+  static constexpr int B = G::T < 32 ? G::T : 32;
+  static constexpr int H = B / 2;          // partner = lane ^ H
+  int jsp, jfq;                            // spatial / frequency butterfly
+  bool isz, ish;                           // jfq == 0 / jfq == S/2
+  unsigned mask;
+  __device__ __forceinline__ FastMap(int t, unsigned group_mask) {
+    const int w = t / B, l = t % B;
+    const int lo = H * w + l;
+    isz = (w == 0 && l == 0);
+    ish = (w == 0 && l == H);
+    jsp = l < H ? lo : S - 1 - H * w - (l - H);
+    jfq = l < H ? lo : (ish ? S / 2 : S - H * w - (l - H));
+    mask = group_mask;
+  }
+  __device__ __forceinline__ float2 xor_shfl(float2 v) const {
+    return make_float2(__shfl_xor_sync(mask, v.x, H), __shfl_xor_sync(mask, v.y, H));
+  }
+  // bins of frequency slot s: lo = jfq + s*S, hi = N - lo (special slot: 0, N/2)
+  __device__ __forceinline__ bool special(int s) const { return s == 0 && isz; }
+  template <class P>
+  __device__ __forceinline__ P* plo(P* a, int s) const { return a + jfq + s * S; }
+  template <class P>
+  __device__ __forceinline__ P* phi(P* a, int s) const {
+    return (s == 0 && isz) ? a + N / 2 : (a + (N - jfq)) - s * S;
+  }
+};
+
+// Z[jfq + q*S] (q < 16, last-pass output) -> W[s] = Z[hi_s] for s < 8.
+template <class G>
+__device__ __forceinline__ void fp_partner(const float2 (&z)[16], float2 (&w)[8], const FastMap<G>& fm) {
+  float2 r[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) r[s] = fm.xor_shfl(z[15 - s]);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const float2 self0 = s == 0 ? z[8] : z[(16 - s) & 15];
+    w[s] = fm.isz ? self0 : (fm.ish ? z[15 - s] : r[s]);
+  }
+}
+
+// G at (lo_s, hi_s) for s < 8 -> v[q] = G[jfq + q*S] (pass-0 inputs).
+template <class G>
+__device__ __forceinline__ void fp_scatter(const float2 (&gl)[8], const float2 (&gh)[8], float2 (&v)[16],
+                                           const FastMap<G>& fm) {
+  float2 r[8];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) r[s] = fm.xor_shfl(gh[s]);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) v[s] = gl[s];
+#pragma unroll
+  for (int q = 8; q < 16; ++q) {
+    const float2 self0 = q == 8 ? gh[0] : gh[16 - q];
+    v[q] = fm.isz ? self0 : (fm.ish ? gh[15 - q] : r[15 - q]);
+  }
+}
+
+__device__ __forceinline__ float2 ld_f2(const float* p) { return __ldg(reinterpret_cast<const float2*>(p)); }
+
+// Pass-0 inputs from two rows (and an optional scale row): the 64-bit pair
+// x[2m], x[2m+1] at m = jsp + q*S (q < 8) holds z[m] (kept) and z[N-1-m]
+// (the partner's slot 15-q, sent).
+template <class G, bool SCALE>
+__device__ __forceinline__ void fp_load(float2 (&v)[16], const float* xa, const float* xb, const float* sc,
+                                        const FastMap<G>& fm) {
+  constexpr int S = FastMap<G>::S;
+  const float* pa = xa + 2 * fm.jsp;
+  const float* pb = (xb ? xb : xa) + 2 * fm.jsp;
+  const float* ps = (SCALE ? sc : xa) + 2 * fm.jsp;
+  float2 snd[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    float2 a2 = ld_f2(pa + 2 * q * S);
+    float2 b2 = xb ? ld_f2(pb + 2 * q * S) : make_float2(0.f, 0.f);
+    if constexpr (SCALE) {
+      const float2 s2 = ld_f2(ps + 2 * q * S);
+      a2 = make_float2(a2.x * s2.x, a2.y * s2.y);
+      b2 = make_float2(b2.x * s2.x, b2.y * s2.y);
+    }
+    v[q] = make_float2(a2.x, b2.x);
+    snd[q] = make_float2(a2.y, b2.y);
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[15 - q] = fm.xor_shfl(snd[q]);
+}
+
+// Last-pass outputs h[q] = H[jsp + q*S] (rowA = H.x, rowB = -H.y) -> the
+// thread's 64-bit output pairs at 2m, m = jsp + q*S (q < 8): (own, partner's
+// slot 15-q).  Returns rowA/rowB pairs in oa/ob.
+template <class G>
+__device__ __forceinline__ void fp_out_pairs(const float2 (&h)[16], float2 (&oa)[8], float2 (&ob)[8],
+                                             const FastMap<G>& fm) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float2 r = fm.xor_shfl(h[15 - q]);
+    oa[q] = make_float2(h[q].x, r.x);
+    ob[q] = make_float2(-h[q].y, -r.y);
+  }
 }
 
 }  // namespace acdc

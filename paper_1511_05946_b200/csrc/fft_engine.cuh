@@ -3,16 +3,23 @@
 // One "row-pair group" of T threads transforms an N-point complex vector whose
 // real and imaginary parts are two independent real rows (A and B).  Each
 // thread holds E complex values in registers; passes are Stockham radix-R
-// (R in {2,4,8,16}) with compile-time internal twiddles, one dynamic twiddle
+// (R in {2,4,8,16}) with compile-time internal twiddles, one table twiddle
 // multiply per element between passes, and a padded shared-memory exchange
-// between passes (1 barrier per exchange when double-buffered).
+// between passes.
 //
-// The Stockham pass (input read at stride N/R, autosorted output) is:
-//   j in [0, N/R), k = j mod Ns
+// Stockham pass p (span Ns = product of earlier radices, input stride N/R):
+//   butterfly j in [0, N/R), k = j mod Ns
 //   a[q] = in[j + q*N/R] * W_{Ns*R}^{q*k}
 //   a    = DFT_R(a)
 //   out[(j-k)*R + k + q'*Ns] = a[q']
 // which after the last pass leaves the DFT in natural order.
+//
+// Addressing discipline: every shared/global address is "per-thread base +
+// compile-time immediate".  Otherwise ptxas CSEs the (thread-invariant)
+// address arithmetic of the two FFTs of a row iteration and keeps dozens of
+// addresses live across the whole iteration, which spills.  This is why the
+// twiddles live in per-pass [q][k] tables and the padding function padi()
+// is split into base and offset parts below.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -25,10 +32,18 @@ __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(
 __device__ __forceinline__ float2 cmul(float2 a, float2 w) {
   return make_float2(fmaf(a.x, w.x, -a.y * w.y), fmaf(a.x, w.y, a.y * w.x));
 }
+__device__ __forceinline__ float2 cmulc(float2 z, float wr, float wi) {
+  return make_float2(fmaf(z.x, wr, -z.y * wi), fmaf(z.x, wi, z.y * wr));
+}
 // -i * z
 __device__ __forceinline__ float2 mul_ni(float2 z) { return make_float2(z.y, -z.x); }
-// +i * z
-__device__ __forceinline__ float2 mul_pi(float2 z) { return make_float2(-z.y, z.x); }
+
+// Global load that ptxas may not hoist across barriers (large-N tables).
+__device__ __forceinline__ float2 ldg_f2_volatile(const float2* p) {
+  float2 r;
+  asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "l"(p));
+  return r;
+}
 
 // Forward-DFT constants: W_R^m = exp(-2 pi i m / R)
 #define ACDC_C1 0.92387953251128675613f  // cos(pi/8)
@@ -52,9 +67,8 @@ __device__ __forceinline__ void dft4(float2& a0, float2& a1, float2& a2, float2&
   a3 = csub(t1, mul_ni(t3));
 }
 
-// z * W8^1 = z * (h, -h)
+// z * W8^1 = z * (h, -h);  z * W8^3 = z * (-h, -h)
 __device__ __forceinline__ float2 mul_w8_1(float2 z) { return make_float2(ACDC_H * (z.x + z.y), ACDC_H * (z.y - z.x)); }
-// z * W8^3 = z * (-h, -h)
 __device__ __forceinline__ float2 mul_w8_3(float2 z) { return make_float2(ACDC_H * (z.y - z.x), -ACDC_H * (z.x + z.y)); }
 
 __device__ __forceinline__ void dft8(float2* a) {
@@ -73,27 +87,23 @@ __device__ __forceinline__ void dft8(float2* a) {
   a[7] = csub(e3, o3);
 }
 
-__device__ __forceinline__ float2 cmulc(float2 z, float wr, float wi) {
-  return make_float2(fmaf(z.x, wr, -z.y * wi), fmaf(z.x, wi, z.y * wr));
-}
-
 __device__ __forceinline__ void dft16(float2* a) {
   // 4 x 4: n = 4 n1 + n2, k = k1 + 4 k2
 #pragma unroll
   for (int n2 = 0; n2 < 4; ++n2) dft4(a[n2], a[n2 + 4], a[n2 + 8], a[n2 + 12]);
   // a[n2 + 4 k1] *= W16^(n2 k1)
-  a[5] = cmulc(a[5], ACDC_C1, -ACDC_S1);   // n2=1,k1=1 : W^1
-  a[9] = mul_w8_1(a[9]);                   // n2=1,k1=2 : W^2
-  a[13] = cmulc(a[13], ACDC_S1, -ACDC_C1); // n2=1,k1=3 : W^3
-  a[6] = mul_w8_1(a[6]);                   // n2=2,k1=1 : W^2
-  a[10] = mul_ni(a[10]);                   // n2=2,k1=2 : W^4
-  a[14] = mul_w8_3(a[14]);                 // n2=2,k1=3 : W^6
-  a[7] = cmulc(a[7], ACDC_S1, -ACDC_C1);   // n2=3,k1=1 : W^3
-  a[11] = mul_w8_3(a[11]);                 // n2=3,k1=2 : W^6
-  a[15] = cmulc(a[15], -ACDC_C1, ACDC_S1); // n2=3,k1=3 : W^9
+  a[5] = cmulc(a[5], ACDC_C1, -ACDC_S1);   // W^1
+  a[9] = mul_w8_1(a[9]);                   // W^2
+  a[13] = cmulc(a[13], ACDC_S1, -ACDC_C1); // W^3
+  a[6] = mul_w8_1(a[6]);                   // W^2
+  a[10] = mul_ni(a[10]);                   // W^4
+  a[14] = mul_w8_3(a[14]);                 // W^6
+  a[7] = cmulc(a[7], ACDC_S1, -ACDC_C1);   // W^3
+  a[11] = mul_w8_3(a[11]);                 // W^6
+  a[15] = cmulc(a[15], -ACDC_C1, ACDC_S1); // W^9
 #pragma unroll
   for (int k1 = 0; k1 < 4; ++k1) dft4(a[4 * k1], a[4 * k1 + 1], a[4 * k1 + 2], a[4 * k1 + 3]);
-  // X[k1 + 4 k2] sits at a[4 k1 + k2]: transpose 4x4
+  // X[k1 + 4 k2] sits at a[4 k1 + k2]: transpose 4x4 (register renaming)
   float2 t[16];
 #pragma unroll
   for (int i = 0; i < 16; ++i) t[i] = a[i];
@@ -105,8 +115,7 @@ __device__ __forceinline__ void dft16(float2* a) {
 
 template <int R>
 __device__ __forceinline__ void dft(float2* a) {
-  if constexpr (R == 1) {
-  } else if constexpr (R == 2) {
+  if constexpr (R == 2) {
     dft2(a[0], a[1]);
   } else if constexpr (R == 4) {
     dft4(a[0], a[1], a[2], a[3]);
@@ -119,24 +128,10 @@ __device__ __forceinline__ void dft(float2* a) {
 }
 
 // ------------------------------------------------------------ geometry
-__host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n >> 1); }
-
-// Per-N compile-time geometry.
+// Radix plan and per-pass twiddle-table layout for N = 2^LOGN (16 x small x 16...).
 template <int LOGN>
-struct Geo {
+struct Plan {
   static constexpr int N = 1 << LOGN;
-  static constexpr int E = LOGN >= 15 ? 32 : (N >= 16 ? 16 : N);  // complex values per thread
-  static constexpr int T = N / E;                                 // threads per row-pair group
-  static constexpr int CTA = T >= 128 ? T : 128;                  // threads per CTA
-  static constexpr int GPC = CTA / T;                             // groups per CTA
-  static constexpr int PADN = N + N / 16;                         // padded float2 slots per buffer
-  static constexpr bool SPLIT = (N >= 32768);                     // exchange re / im separately
-  static constexpr int NBUF = (N >= 8192) ? 1 : 2;                // double-buffered exchanges
-  static constexpr int BUF_FLOATS = SPLIT ? PADN : 2 * PADN;      // floats per buffer
-  static constexpr int SMEM_BYTES = GPC * NBUF * BUF_FLOATS * 4;
-  // resident CTAs per SM requested from ptxas (caps registers at 64K / (CTA * MINB))
-  static constexpr int MINB = CTA >= 512 ? 1 : 512 / CTA;
-  // radix plan: 16 x small x 16 x 16 ...   (LOGN = 4a + r)
   static constexpr int A16 = LOGN / 4;
   static constexpr int REM = LOGN % 4;
   static constexpr int NPASS = LOGN < 4 ? 1 : A16 + (REM ? 1 : 0);
@@ -146,9 +141,67 @@ struct Geo {
   __host__ __device__ static constexpr int span(int p) {  // Ns before pass p
     return p == 0 ? 1 : span(p - 1) * radix(p - 1);
   }
+  // pass p >= 1 twiddles W_{Ns R}^{q k}, stored at tw_off(p) + (q-1)*Ns + k
+  __host__ __device__ static constexpr int tw_off(int p) {
+    return p <= 1 ? 0 : tw_off(p - 1) + (radix(p - 1) - 1) * span(p - 1);
+  }
+  static constexpr int TW_ENTRIES = tw_off(NPASS);  // float2 entries (0 for one pass)
+  static constexpr int CP_ENTRIES = N / 2 + 1;      // DCT post-twiddles c'_k
 };
 
-__device__ __forceinline__ int padi(int i) { return i + (i >> 4); }
+// Per-N compile-time geometry and shared-memory plan.
+//
+// STASH = floats per thread of per-group scratch the kernel needs besides the
+// exchange buffers (the backward keeps g3 and grad_a partials there).  CTAs
+// hold GPC row-pair groups (512 threads when T <= 512) sharing one copy of the
+// tables; the plan prefers tables in smem and double-buffered exchanges and
+// falls back (single buffer, tables in global) until the CTA fits in 227 KB.
+template <int LOGN, int STASH = 0>
+struct Geo : Plan<LOGN> {
+  using P_ = Plan<LOGN>;
+  static constexpr int N = 1 << LOGN;
+  static constexpr int E = LOGN >= 15 ? 32 : (N >= 16 ? 16 : N);  // complex values per thread
+  static constexpr int T = N / E;                                 // threads per row-pair group
+  static constexpr int GPC = T <= 512 ? 512 / T : 1;              // groups per CTA
+  static constexpr int CTA = T * GPC;                             // threads per CTA
+  static constexpr int PADN = N + N / 16;                         // padded float2 slots per buffer
+  static constexpr bool SPLIT = (N >= 32768);                     // exchange re / im separately
+  static constexpr int BUF_FLOATS = SPLIT ? PADN : 2 * PADN;      // floats per exchange buffer
+  static constexpr int STASH_FLOATS = STASH * T;                  // per group
+  static constexpr int SMEM_LIMIT = 227 * 1024;
+  static constexpr int TAB_FULL = (2 * (P_::TW_ENTRIES + P_::CP_ENTRIES) + 3) & ~3;
+  __host__ __device__ static constexpr int bytes(bool tab, int nbuf, bool stash) {
+    return 4 * ((tab ? TAB_FULL : 0) + GPC * (nbuf * BUF_FLOATS + (stash ? STASH_FLOATS : 0)));
+  }
+  // the stash goes to global scratch only if it cannot fit beside one buffer
+  static constexpr bool STASH_SMEM = bytes(false, 1, true) <= SMEM_LIMIT;
+  static constexpr bool FIT_T2 = !SPLIT && bytes(true, 2, STASH_SMEM) <= SMEM_LIMIT;
+  static constexpr bool FIT_T1 = bytes(true, 1, STASH_SMEM) <= SMEM_LIMIT;
+  static constexpr bool FIT_G2 = !SPLIT && bytes(false, 2, STASH_SMEM) <= SMEM_LIMIT;
+  static constexpr bool TW_SMEM = FIT_T2 || FIT_T1;  // tables staged in smem?
+  static constexpr int NBUF = FIT_T2 ? 2 : (FIT_T1 ? 1 : (FIT_G2 ? 2 : 1));
+  static constexpr int TAB_FLOATS = TW_SMEM ? TAB_FULL : 0;
+  static constexpr int SMEM_BYTES = bytes(TW_SMEM, NBUF, STASH_SMEM);
+  static constexpr int GROUP_FLOATS = NBUF * BUF_FLOATS + (STASH_SMEM ? STASH_FLOATS : 0);
+  // fast-pairing path (dct_pair.cuh): one radix-16 butterfly per thread in
+  // the first and last pass
+  static constexpr bool FP = E == 16 && N >= 256 && P_::NPASS >= 2 && P_::radix(0) == 16 &&
+                             P_::radix(P_::NPASS - 1) == 16 && T == N / 16;
+  // global scratch floats per group when the stash does not fit in smem
+  static constexpr int GSCRATCH_FLOATS = STASH_SMEM ? 0 : STASH_FLOATS;
+#ifdef ACDC_MINB_OVERRIDE
+  static constexpr int MINB = ACDC_MINB_OVERRIDE;
+#else
+  static constexpr int MINB = 1;  // 512-thread CTAs: 128 registers per thread
+#endif
+};
+
+// Padded exchange index (one float2 of padding per 16 slots).  For a
+// power-of-two stride S and base j < S (or S, j multiples of 16):
+//   padi(j + q*S) = padi(j) + padoff(q*S)
+// which lets every exchange address be a base register plus an immediate.
+__host__ __device__ constexpr int padi(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int padoff(int off) { return off + (off >> 4); }
 
 // Group-local barrier: warp mask for T <= 32, named barrier otherwise.
 template <class G>
@@ -158,7 +211,7 @@ struct GroupSync {
   __device__ __forceinline__ GroupSync(int grp) {
     if constexpr (G::T < 32) {
       int lane = threadIdx.x & 31;
-      mask = ((G::T == 32 ? 0xffffffffu : ((1u << G::T) - 1u)) << (lane & ~(G::T - 1)));
+      mask = ((1u << G::T) - 1u) << (lane & ~(G::T - 1));
     } else {
       mask = 0xffffffffu;
     }
@@ -168,56 +221,45 @@ struct GroupSync {
     if constexpr (G::T <= 32) {
       __syncwarp(mask);
     } else if constexpr (G::GPC == 1) {
-      __syncthreads();
+      asm volatile("bar.sync 0;" ::: "memory");
     } else {
       asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(G::T) : "memory");
     }
   }
 };
 
-// ------------------------------------------------------------ Stockham passes
-// Compute pass P in registers (twiddle + DFT_R).  v[b*R + q] holds
-// in[j_b + q*N/R] for butterfly j_b = t + b*T.
-template <class G, int P>
-__device__ __forceinline__ void pass_compute(float2 (&v)[G::E], const float2* __restrict__ tw, int t) {
-  constexpr int R = G::radix(P);
-  constexpr int NS = G::span(P);
-  constexpr int NB = G::E / R;
-#pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    if constexpr (NS > 1) {
-      const int j = t + b * G::T;
-      const int k = j & (NS - 1);
-      constexpr int S = G::N / (NS * R);
-      const int base = k * S;
-#pragma unroll
-      for (int q = 1; q < R; ++q) v[b * R + q] = cmul(v[b * R + q], __ldg(&tw[q * base]));
-    }
-    dft<R>(&v[b * R]);
+// Table read: shared memory (ordered by the group barriers) or, for large N,
+// a non-hoistable global load.
+template <class G>
+__device__ __forceinline__ float2 tab_load(const float2* tab, int i) {
+  if constexpr (G::TW_SMEM) {
+    return tab[i];
+  } else {
+    return ldg_f2_volatile(tab + i);
   }
 }
 
 // ------------------------------------------------------------ exchanges
-// Element accessors for one exchange: full float2 slots, or one component
-// (re or im) at a time when the buffer only holds N floats (SPLIT mode).
+// Element accessors for one exchange, taking PADDED indices: full float2
+// slots, or one component at a time when the buffer holds N floats (SPLIT).
 struct PutFull {
   float2* b;
-  __device__ __forceinline__ void operator()(int i, float2 v) const { b[padi(i)] = v; }
+  __device__ __forceinline__ void operator()(int pi, float2 v) const { b[pi] = v; }
 };
 struct GetFull {
   const float2* b;
-  __device__ __forceinline__ void operator()(int i, float2& d) const { d = b[padi(i)]; }
+  __device__ __forceinline__ void operator()(int pi, float2& d) const { d = b[pi]; }
 };
 struct PutComp {
   float* b;
   int c;
-  __device__ __forceinline__ void operator()(int i, float2 v) const { b[padi(i)] = c ? v.y : v.x; }
+  __device__ __forceinline__ void operator()(int pi, float2 v) const { b[pi] = c ? v.y : v.x; }
 };
 struct GetComp {
   const float* b;
   int c;
-  __device__ __forceinline__ void operator()(int i, float2& d) const {
-    float f = b[padi(i)];
+  __device__ __forceinline__ void operator()(int pi, float2& d) const {
+    float f = b[pi];
     if (c) d.y = f; else d.x = f;
   }
 };
@@ -256,67 +298,93 @@ __device__ __forceinline__ void xchg(Xbuf<G>& xb, const GroupSync<G>& gs, WF&& w
   }
 }
 
-// Write the outputs of pass P at their autosorted positions.
-template <class G, int P, class PUT>
-__device__ __forceinline__ void pass_store(const float2 (&v)[G::E], const PUT& put, int t) {
+// ------------------------------------------------------------ Stockham passes
+// The thread's butterflies in pass P are j0 + b*T (b < E/R).  Normally j0 = t;
+// the fast-pairing path (dct_pair.cuh) remaps j0 in the first and last pass.
+// All inputs/outputs are addressed as padi(j0) + padoff(b*T) + padoff(q*S).
+
+// Compute pass P in registers (table twiddle + DFT_R).
+template <class G, int P>
+__device__ __forceinline__ void pass_compute(float2 (&v)[G::E], const float2* tw, int j0) {
   constexpr int R = G::radix(P);
   constexpr int NS = G::span(P);
   constexpr int NB = G::E / R;
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
-    const int j = t + b * G::T;
-    const int k = j & (NS - 1);
-    const int d = (j - k) * R + k;
+    if constexpr (NS > 1) {
+      const int k = (j0 + b * G::T) & (NS - 1);
+      const float2* row = tw + G::tw_off(P) + k;  // row[(q-1)*NS] = W_{NS R}^{q k}
 #pragma unroll
-    for (int q = 0; q < R; ++q) put(d + q * NS, v[b * R + q]);
+      for (int q = 1; q < R; ++q) v[b * R + q] = cmul(v[b * R + q], tab_load<G>(row, (q - 1) * NS));
+    }
+    dft<R>(&v[b * R]);
+  }
+}
+
+// Write the outputs of pass P at their autosorted positions.
+template <class G, int P, class PUT>
+__device__ __forceinline__ void pass_store(const float2 (&v)[G::E], const PUT& put, int j0) {
+  constexpr int R = G::radix(P);
+  constexpr int NS = G::span(P);
+  constexpr int NB = G::E / R;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int j = j0 + b * G::T;
+    const int k = j & (NS - 1);
+    const int pd = padi((j - k) * R + k);
+#pragma unroll
+    for (int q = 0; q < R; ++q) put(pd + padoff(q * NS), v[b * R + q]);
   }
 }
 
 // Read the inputs of pass P (stride N/R).
 template <class G, int P, class GET>
-__device__ __forceinline__ void pass_load(float2 (&v)[G::E], const GET& get, int t) {
+__device__ __forceinline__ void pass_load(float2 (&v)[G::E], const GET& get, int j0) {
   constexpr int R = G::radix(P);
   constexpr int NB = G::E / R;
-  constexpr int STRIDE = G::N / R;
+  constexpr int S = G::N / R;
+  const int pt = padi(j0);
 #pragma unroll
-  for (int b = 0; b < NB; ++b) {
-    const int j = t + b * G::T;
+  for (int b = 0; b < NB; ++b)
 #pragma unroll
-    for (int q = 0; q < R; ++q) get(j + q * STRIDE, v[b * R + q]);
-  }
+    for (int q = 0; q < R; ++q) get(pt + padoff(b * G::T) + padoff(q * S), v[b * R + q]);
 }
 
 // All passes of the FFT; v holds pass-0 inputs on entry and the natural-order
-// outputs of the last pass on exit (v[b*R_L + q] = X[j_b + q*N/R_L]).
+// outputs of the last pass on exit (v[b*R_L + q] = X[j_b + q*N/R_L]).  Pass 0
+// uses butterfly base jf, the last pass jl, the others t.
 template <class G, int P = 0>
 __device__ __forceinline__ void fft_passes(float2 (&v)[G::E], Xbuf<G>& xb, const GroupSync<G>& gs,
-                                           const float2* __restrict__ tw, int t) {
-  pass_compute<G, P>(v, tw, t);
-  if constexpr (P + 1 < G::NPASS) {
+                                           const float2* tw, int t, int jf, int jl) {
+  constexpr int L = G::NPASS - 1;
+  const int jp = P == 0 ? jf : (P == L ? jl : t);
+  pass_compute<G, P>(v, tw, jp);
+  if constexpr (P < L) {
+    constexpr int PN = P + 1;
+    const int jn = PN == L ? jl : t;
     xchg(
-        xb, gs, [&](const auto& put) { pass_store<G, P>(v, put, t); },
-        [&](const auto& get) { pass_load<G, P + 1>(v, get, t); });
-    fft_passes<G, P + 1>(v, xb, gs, tw, t);
+        xb, gs, [&](const auto& put) { pass_store<G, P>(v, put, jp); },
+        [&](const auto& get) { pass_load<G, PN>(v, get, jn); });
+    fft_passes<G, PN>(v, xb, gs, tw, t, jf, jl);
   }
 }
-
-// Position n of the last-pass output slot (b, q).
 template <class G>
-__device__ __forceinline__ int last_pos(int t, int b, int q) {
-  constexpr int R = G::radix(G::NPASS - 1);
-  return t + b * G::T + q * (G::N / R);
-}
-// Position m of the first-pass input slot (b, q).
-template <class G>
-__device__ __forceinline__ int first_pos(int t, int b, int q) {
-  constexpr int R = G::radix(0);
-  return t + b * G::T + q * (G::N / R);
+__device__ __forceinline__ void fft_passes(float2 (&v)[G::E], Xbuf<G>& xb, const GroupSync<G>& gs,
+                                           const float2* tw, int t) {
+  fft_passes<G, 0>(v, xb, gs, tw, t, t, t);
 }
 
-// Makhoul reorder: packed index m -> signal index (transforms.py:109-113)
-template <int N>
-__device__ __forceinline__ int reorder_src(int m) {
-  return m < N / 2 ? 2 * m : 2 * (N - 1 - m) + 1;
-}
+// Makhoul reorder (transforms.py:109-113): packed index m -> signal index
+// src = 2m (m < N/2) or 2(N-1-m)+1.  For the first/last-pass slot (b, q) of
+// thread t, m = t + b*T + q*N/R lies in the lower half iff q < R/2, so
+//   q <  R/2:  src = 2t         + off(b, q)
+//   q >= R/2:  src = (2N-1-2t)  - off(b, q),   off = 2(b*T + q*N/R)
+template <class G, int P>
+struct RowMap {
+  static constexpr int R = G::radix(P);
+  static constexpr int NB = G::E / R;
+  __host__ __device__ static constexpr bool lower(int q) { return 2 * q < R; }
+  __host__ __device__ static constexpr int off(int b, int q) { return 2 * (b * G::T + q * (G::N / R)); }
+};
 
 }  // namespace acdc
