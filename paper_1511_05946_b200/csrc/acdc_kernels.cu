@@ -294,15 +294,115 @@ __global__ void ACDC_LB(GeoBwd<LOGN>) acdc_bwd_kernel(KParams p) {
   float* st_ga = sbase + 2 * E * T + t;                  // [E][T]
   const float2 *tw, *cp;
   stage_tables<G>(p, smem_f, tw, cp);
-  const Slots<G> sl(t);
   float acc_d[E], acc_b[E];
 #pragma unroll
   for (int i = 0; i < E; ++i) {
     acc_d[i] = acc_b[i] = 0.f;
     st_ga[i * T] = 0.f;
   }
-
   const int64_t npairs = (p.rows + 1) >> 1;
+
+  if constexpr (G::FP) {
+    // acc_b/acc_d[2s], [2s+1]: bins lo_s, hi_s;  st_ga[2q], [2q+1]: positions
+    // 2m, 2m+1 with m = jsp + q*S;  st_g3[2s], [2s+1]: g3 at lo_s, hi_s.
+    constexpr int S = FastMap<G>::S;
+    const FastMap<G> fm(t, gs.mask);
+    for (int64_t rp = c.gid; rp < npairs; rp += c.gstride) {
+      const int64_t ra = 2 * rp;
+      const bool hasb = ra + 1 < p.rows;
+      const float* xa = p.x + ra * p.ldx;
+      const float* xbp = hasb ? p.x + (ra + 1) * p.ldx : nullptr;
+      if (t == 0 && rp + c.gstride < npairs) {  // next row pair -> L2
+        const int64_t nr = 2 * (rp + c.gstride);
+        prefetch_row_l2(p.dy + nr * p.ldy, G::N);
+        prefetch_row_l2(p.x + nr * p.ldx, G::N);
+        if (nr + 1 < p.rows) {
+          prefetch_row_l2(p.dy + (nr + 1) * p.ldy, G::N);
+          prefetch_row_l2(p.x + (nr + 1) * p.ldx, G::N);
+        }
+      }
+      float2 v[16];
+      const float2 chi = tab_load<G>(cp, G::N / 2);
+      // g3 = C2(dy): grad_bias partial, stash
+      fp_load<G, false>(v, p.dy + ra * p.ldy, hasb ? p.dy + (ra + 1) * p.ldy : nullptr, nullptr, fm);
+      fft_passes<G, 0>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
+      {
+        float2 w[8];
+        fp_partner<G>(v, w, fm);
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          float2 gl, gh;
+          dct2_post(v[s], w[s], tab_load<G>(fm.plo(cp, s), 0), fm.special(s), chi, gl, gh);
+          acc_b[2 * s] += gl.x + gl.y;
+          acc_b[2 * s + 1] += gh.x + gh.y;
+          st_g3[(2 * s) * T] = gl;
+          st_g3[(2 * s + 1) * T] = gh;
+        }
+      }
+      // h2 = C2(a*x): grad_d partial; Y = d * g3 -> DCT-III pre-pass
+      fp_load<G, true>(v, xa, xbp, p.a, fm);
+      fft_passes<G, 0>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
+      {
+        float2 w[8], gl[8], gh[8];
+        fp_partner<G>(v, w, fm);
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const float2 cs = tab_load<G>(fm.plo(cp, s), 0);
+          float2 hl, hh;
+          dct2_post(v[s], w[s], cs, fm.special(s), chi, hl, hh);
+          const float2 g3l = st_g3[(2 * s) * T], g3h = st_g3[(2 * s + 1) * T];
+          acc_d[2 * s] = fmaf(hl.x, g3l.x, fmaf(hl.y, g3l.y, acc_d[2 * s]));
+          acc_d[2 * s + 1] = fmaf(hh.x, g3h.x, fmaf(hh.y, g3h.y, acc_d[2 * s + 1]));
+          const float dl = ld_plain(fm.plo(p.d, s)), dh = ld_plain(fm.phi(p.d, s));
+          dct3_pre(make_float2(g3l.x * dl, g3l.y * dl), make_float2(g3h.x * dh, g3h.y * dh), cs, fm.special(s), chi,
+                   gl[s], gh[s]);
+        }
+        fp_scatter<G>(gl, gh, v, fm);
+      }
+      // g1 = C3(d * g3); dx = a * g1; grad_a partial += x * g1
+      fft_passes<G, 0>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
+      float2 ga[8], gb[8];
+      fp_out_pairs<G>(v, ga, gb, fm);
+      const int64_t rb = hasb ? ra + 1 : ra;
+      float2* oa = reinterpret_cast<float2*>(p.y + ra * p.ldo + 2 * fm.jsp);
+      float2* ob = reinterpret_cast<float2*>(p.y + rb * p.ldo + 2 * fm.jsp);
+      const float* pxa = xa + 2 * fm.jsp;
+      const float* pxb = p.x + rb * p.ldx + 2 * fm.jsp;
+      const float* pa = p.a + 2 * fm.jsp;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float2 av = ld_f2(pa + 2 * q * S);
+        const float2 xav = ld_f2(pxa + 2 * q * S);
+        float s0 = ga[q].x * xav.x, s1 = ga[q].y * xav.y;
+        oa[q * S] = make_float2(av.x * ga[q].x, av.y * ga[q].y);
+        if (hasb) {
+          const float2 xbv = ld_f2(pxb + 2 * q * S);
+          s0 = fmaf(gb[q].x, xbv.x, s0);
+          s1 = fmaf(gb[q].y, xbv.y, s1);
+          ob[q * S] = make_float2(av.x * gb[q].x, av.y * gb[q].y);
+        }
+        st_ga[(2 * q) * T] += s0;
+        st_ga[(2 * q + 1) * T] += s1;
+      }
+    }
+    // per-group partials
+    float* w = p.ws + c.gid * 3 * G::N;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      w[2 * (fm.jsp + q * S)] = st_ga[(2 * q) * T];
+      w[2 * (fm.jsp + q * S) + 1] = st_ga[(2 * q + 1) * T];
+    }
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      *fm.plo(w + G::N, s) = acc_d[2 * s];
+      *fm.phi(w + G::N, s) = acc_d[2 * s + 1];
+      *fm.plo(w + 2 * G::N, s) = acc_b[2 * s];
+      *fm.phi(w + 2 * G::N, s) = acc_b[2 * s + 1];
+    }
+    return;
+  }
+
+  const Slots<G> sl(t);
   for (int64_t rp = c.gid; rp < npairs; rp += c.gstride) {
     const int64_t ra = 2 * rp;
     const bool hasb = ra + 1 < p.rows;
