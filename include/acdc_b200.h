@@ -25,6 +25,8 @@
  *   acdc_dct2_f32  dct(plan, x)  / kernels.dct2_batch transforms.py:137-145, _kernels.pyx:60-73
  *   acdc_dct3_f32  idct(plan, y) / kernels.dct3_batch transforms.py:148-156, _kernels.pyx:76-91
  *   acdc_prepare   DctPlan(n, mode="fast") table build transforms.py:86-122
+ *   afdf_fwd_c64   AfdfLayer.forward                 layers.py:199-204
+ *   afdf_bwd_c64   AfdfLayer.backward (accumulates)  layers.py:206-215
  */
 #ifndef ACDC_B200_H
 #define ACDC_B200_H
@@ -81,6 +83,21 @@ int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, con
 /* Row-wise orthonormal DCT-II / DCT-III (the reference dct / idct). */
 int acdc_dct2_f32(const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream);
 int acdc_dct3_f32(const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream);
+
+/* ---- AFDF: complex diagonals around the FFT pair (layers.py:159-215) ----
+ * Rows are complex64, interleaved (re, im); ld in complex elements; a, d, grads
+ * are n complex values.  2 <= n <= 16384, 8-byte aligned pointers.
+ *   afdf_fwd_c64:  y = IFFT(d * FFT(a * x))        (FFT unnormalised, IFFT 1/n;
+ *                                                    transforms.py:166-179)
+ *   afdf_bwd_c64:  g3 = FFT(dy)/n; grad_d (+)= sum g3 * conj(FFT(a*x));
+ *                  g1 = n * IFFT(g3 * conj(d)); grad_a (+)= sum g1 * conj(x);
+ *                  dx = g1 * conj(a)             (gradient = dL/dRe + i dL/dIm) */
+int afdf_fwd_c64(const float* x, float* y, const float* a, const float* d, int64_t rows, int32_t n, int64_t ldx,
+                 int64_t ldy, acdc_stream_t stream);
+size_t afdf_bwd_workspace_bytes(int64_t rows, int32_t n);
+int afdf_bwd_c64(const float* x, const float* dy, float* dx, const float* a, const float* d, float* grad_a,
+                 float* grad_d, int accumulate, void* ws, size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx,
+                 int64_t ldy, int64_t lddx, acdc_stream_t stream);
 
 #ifdef __cplusplus
 }

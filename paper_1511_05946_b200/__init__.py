@@ -7,9 +7,22 @@ No CPU fallback: without ``libacdc_b200.so`` (``python -m
 paper_1511_05946_b200.build``) and a CUDA device, every numeric call raises.
 """
 
-from .functional import AcdcFunction, acdc, acdc_backward, acdc_forward, dct, idct, prepare
+from .functional import (
+    AcdcFunction,
+    AfdfFunction,
+    acdc,
+    acdc_backward,
+    acdc_forward,
+    afdf,
+    afdf_backward,
+    afdf_forward,
+    dct,
+    idct,
+    prepare,
+)
 from .layers import (
     AcdcLayer,
+    AfdfLayer,
     Cascade,
     DenseLayer,
     Layer,
@@ -17,6 +30,7 @@ from .layers import (
     PermutationLayer,
     ReluLayer,
     acdc_cascade,
+    afdf_cascade,
     count_params,
 )
 

@@ -21,14 +21,8 @@
 #include <tuple>
 #include <vector>
 
-#include "../../include/acdc_b200.h"
 #include "dct_pair.cuh"
-
-#ifdef ACDC_NO_LB  // experiments: report the natural register demand
-#define ACDC_LB(G)
-#else
-#define ACDC_LB(G) __launch_bounds__(G::CTA, G::MINB)
-#endif
+#include "runtime.h"
 
 namespace acdc {
 
@@ -630,104 +624,28 @@ __global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __re
 
 // ---------------------------------------------------------------- host side
 
-struct Tables {
-  float2* tab = nullptr;  // [pass twiddles W_{Ns R}^{q k} | c'_k = s_k e^{-i pi k/2N}/2, k <= N/2]
-};
-
-static std::mutex g_mu;
-static std::map<std::pair<int, int>, Tables> g_tables;
-static thread_local char g_errbuf[256];
-static thread_local const char* g_last_error = "";
-
-static int set_cuda_error(cudaError_t e) {
-  snprintf(g_errbuf, sizeof(g_errbuf), "CUDA error: %s", cudaGetErrorString(e));
-  g_last_error = g_errbuf;
-  return ACDC_E_CUDA;
-}
-
-// exp(-2 pi i m / M) in double, rounded once to fp32
-static float2 twiddle(long m, long M) {
-  const double pi = 3.14159265358979323846264338327950288;
-  m %= M;
-  const double th = 2.0 * pi * (double)m / (double)M;
-  return make_float2((float)std::cos(th), (float)-std::sin(th));
-}
-
-// Host mirror of Plan<LOGN> (radix 16 x small x 16 ...).
-static void host_plan(int logn, std::vector<int>& radix) {
-  radix.clear();
-  const int n = 1 << logn;
-  if (logn < 4) {
-    radix.push_back(n);
-    return;
-  }
-  const int a16 = logn / 4, rem = logn % 4;
-  const int np = a16 + (rem ? 1 : 0);
-  for (int p = 0; p < np; ++p) radix.push_back((rem && p == 1) ? (1 << rem) : 16);
-}
-
-static int get_tables(int logn, Tables* out) {
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return set_cuda_error(e);
-  std::lock_guard<std::mutex> lk(g_mu);
-  auto key = std::make_pair(dev, logn);
-  auto it = g_tables.find(key);
-  if (it != g_tables.end()) {
-    *out = it->second;
-    return ACDC_OK;
-  }
-  const int n = 1 << logn;
-  std::vector<int> radix;
-  host_plan(logn, radix);
-  std::vector<float2> h;
-  long ns = radix[0];
-  for (size_t p = 1; p < radix.size(); ++p) {
-    const int r = radix[p];
-    for (int q = 1; q < r; ++q)
-      for (long k = 0; k < ns; ++k) h.push_back(twiddle((long)q * k, ns * r));
-    ns *= r;
-  }
-  const double pi = 3.14159265358979323846264338327950288;
-  for (int k = 0; k <= n / 2; ++k) {
-    const double s = (k == 0 ? std::sqrt(1.0 / n) : std::sqrt(2.0 / n)) * 0.5;
-    const double th = pi * (double)k / (2.0 * n);
-    h.push_back(make_float2((float)(s * std::cos(th)), (float)(-s * std::sin(th))));
-  }
-  Tables tb;
-  if ((e = cudaMalloc(&tb.tab, sizeof(float2) * h.size())) != cudaSuccess) return set_cuda_error(e);
-  if ((e = cudaMemcpy(tb.tab, h.data(), sizeof(float2) * h.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
-    return set_cuda_error(e);
-  g_tables[key] = tb;
-  *out = tb;
-  return ACDC_OK;
-}
-
 enum Kind { K_FWD = 0, K_BWD = 1, K_DCT2 = 2, K_DCT3 = 3 };
-
-struct LaunchInfo {
-  const void* fn;
-  int cta;
-  int gpc;
-  int scratch;  // global scratch floats per group (bwd)
-  int smem;
-};
 
 template <int LOGN>
 static LaunchInfo info_for(int kind) {
   using G = Geo<LOGN>;
   using GB = GeoBwd<LOGN>;
-  const void* fn = kind == K_FWD    ? (const void*)acdc_fwd_kernel<LOGN>
-                   : kind == K_BWD  ? (const void*)acdc_bwd_kernel<LOGN>
-                   : kind == K_DCT2 ? (const void*)acdc_dct2_kernel<LOGN>
-                                    : (const void*)acdc_dct3_kernel<LOGN>;
-  return LaunchInfo{fn, G::CTA, G::GPC, kind == K_BWD ? GB::GSCRATCH_FLOATS : 0, kind == K_BWD ? GB::SMEM_BYTES : G::SMEM_BYTES};
+  LaunchInfo li;
+  li.fn = kind == K_FWD    ? (const void*)acdc_fwd_kernel<LOGN>
+          : kind == K_BWD  ? (const void*)acdc_bwd_kernel<LOGN>
+          : kind == K_DCT2 ? (const void*)acdc_dct2_kernel<LOGN>
+                           : (const void*)acdc_dct3_kernel<LOGN>;
+  li.cta = G::CTA;
+  li.gpc = G::GPC;
+  li.scratch = kind == K_BWD ? GB::GSCRATCH_FLOATS : 0;
+  li.smem = kind == K_BWD ? GB::SMEM_BYTES : G::SMEM_BYTES;
+  return li;
 }
 
 static int launch_info(int logn, int kind, LaunchInfo* li) {
   switch (logn) {
-#define ACDC_CASE(L) \
-  case L:            \
+#define ACDC_CASE(L)         \
+  case L:                    \
     *li = info_for<L>(kind); \
     return ACDC_OK;
 #ifndef ACDC_ONLY_LOGN  // experiments: build a single size
@@ -755,65 +673,15 @@ static int launch_info(int logn, int kind, LaunchInfo* li) {
   }
 }
 
-// Persistent-grid size for a kernel: min(groups needed, resident groups).
-struct GridCache {
-  int blocks_per_sm;
-  int sms;
-};
-static std::map<std::tuple<int, int, int>, GridCache> g_grid;
-
-static int grid_for(int logn, int kind, int64_t rows, LaunchInfo* li, int64_t* grid) {
+static int sized(int logn, int kind, int64_t rows, LaunchInfo* li, int64_t* grid) {
   int rc = launch_info(logn, kind, li);
   if (rc) return rc;
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return set_cuda_error(e);
-  GridCache gc;
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    auto key = std::make_tuple(dev, logn, kind);
-    auto it = g_grid.find(key);
-    if (it == g_grid.end()) {
-      if (li->smem > 48 * 1024) {
-        e = cudaFuncSetAttribute(li->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, li->smem);
-        if (e != cudaSuccess) return set_cuda_error(e);
-      }
-      int bps = 0;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, li->fn, li->cta, li->smem);
-      if (e != cudaSuccess) return set_cuda_error(e);
-      int sms = 0;
-      e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      if (e != cudaSuccess) return set_cuda_error(e);
-      if (bps < 1) bps = 1;
-      gc = GridCache{bps, sms};
-      g_grid[key] = gc;
-    } else {
-      gc = it->second;
-    }
-  }
-  const int64_t npairs = (rows + 1) / 2;
-  const int64_t need = (npairs + li->gpc - 1) / li->gpc;
-  const int64_t cap = (int64_t)gc.blocks_per_sm * gc.sms;
-  *grid = need < cap ? need : cap;
-  if (*grid < 1) *grid = 1;
-  return ACDC_OK;
+  return grid_for(*li, (rows + 1) / 2, grid);
 }
 
-static int check_n(int32_t n, int* logn) {
-  if (n < 1 || (n & (n - 1)) != 0) {
-    snprintf(g_errbuf, sizeof(g_errbuf), "fast DCT requires a power-of-two size, got %d", n);
-    g_last_error = g_errbuf;
-    return ACDC_E_SIZE;
-  }
-  int l = 0;
-  while ((1 << l) < n) ++l;
-  if (l > 15) {
-    snprintf(g_errbuf, sizeof(g_errbuf), "size %d exceeds the on-chip limit 32768", n);
-    g_last_error = g_errbuf;
-    return ACDC_E_SIZE;
-  }
-  *logn = l;
-  return ACDC_OK;
+// Rows of n >= 256 are moved as 64-bit pairs: pointers 8-byte aligned, even ld.
+static bool pair_aligned(int32_t n, const void* p, int64_t ld) {
+  return n < 256 || (((uintptr_t)p & 7) == 0 && (ld & 1) == 0);
 }
 
 static int run(int kind, KParams p, int32_t n, cudaStream_t st) {
@@ -826,11 +694,8 @@ static int run(int kind, KParams p, int32_t n, cudaStream_t st) {
   p.tab = tb.tab;
   LaunchInfo li;
   int64_t grid;
-  if ((rc = grid_for(logn, kind, p.rows, &li, &grid))) return rc;
-  void* args[] = {&p};
-  cudaError_t e = cudaLaunchKernel(li.fn, dim3((unsigned)grid), dim3(li.cta), args, li.smem, st);
-  if (e != cudaSuccess) return set_cuda_error(e);
-  return ACDC_OK;
+  if ((rc = sized(logn, kind, p.rows, &li, &grid))) return rc;
+  return launch(li, grid, &p, st);
 }
 
 }  // namespace acdc
@@ -839,32 +704,6 @@ using namespace acdc;
 
 // ==================================================================== C ABI
 extern "C" {
-
-int acdc_abi_version(void) { return ACDC_ABI_VERSION; }
-
-const char* acdc_strerror(int code) {
-  switch (code) {
-    case ACDC_OK:
-      return "ok";
-    case ACDC_E_SIZE:
-    case ACDC_E_CUDA:
-      return g_last_error[0] ? g_last_error : (code == ACDC_E_SIZE ? "unsupported size" : "CUDA error");
-    case ACDC_E_SHAPE:
-      return "invalid shape or leading dimension";
-    case ACDC_E_ALIGN:
-      return "misaligned pointer";
-    case ACDC_E_WS:
-      return "workspace too small";
-    case ACDC_E_NULL:
-      return "null pointer argument";
-    default:
-      return "unknown error";
-  }
-}
-
-const char* acdc_last_error(void) { return g_last_error; }
-
-int acdc_max_n(void) { return 32768; }
 
 int acdc_prepare(int32_t n) {
   int logn;
@@ -876,7 +715,7 @@ int acdc_prepare(int32_t n) {
   for (int k = 0; k < 4; ++k) {
     LaunchInfo li;
     int64_t grid;
-    if ((rc = grid_for(logn, k, 2, &li, &grid))) return rc;
+    if ((rc = sized(logn, k, 2, &li, &grid))) return rc;
   }
   return ACDC_OK;
 }
@@ -892,6 +731,7 @@ int acdc_fwd_f32(const float* x, float* y, const float* a, const float* d, const
   int rc = check_common(x, y, rows, n, ldx, ldy);
   if (rc) return rc;
   if (!a || !d || !bias) return ACDC_E_NULL;
+  if (!pair_aligned(n, x, ldx) || !pair_aligned(n, y, ldy) || !pair_aligned(n, a, 0)) return ACDC_E_ALIGN;
   KParams p{};
   p.x = x;
   p.y = y;
@@ -919,7 +759,7 @@ size_t acdc_bwd_workspace_bytes(int64_t rows, int32_t n) {
   if (logn == 0) return 3 * sizeof(float);
   LaunchInfo li;
   int64_t grid;
-  if (grid_for(logn, K_BWD, rows > 0 ? rows : 1, &li, &grid)) return 0;
+  if (sized(logn, K_BWD, rows > 0 ? rows : 1, &li, &grid)) return 0;
   return (size_t)grid * li.gpc * (3 * (size_t)n + (size_t)li.scratch) * sizeof(float);
 }
 
@@ -930,6 +770,8 @@ int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, con
   if (rc) return rc;
   if (ldy < n) return ACDC_E_SHAPE;
   if (!a || !d || !grad_a || !grad_d || !grad_bias || (rows > 0 && !dy)) return ACDC_E_NULL;
+  if (!pair_aligned(n, x, ldx) || !pair_aligned(n, dy, ldy) || !pair_aligned(n, dx, lddx) || !pair_aligned(n, a, 0))
+    return ACDC_E_ALIGN;
   int logn;
   if ((rc = check_n(n, &logn))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -948,12 +790,6 @@ int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, con
   p.ldy = ldy;
   p.ldo = lddx;
   int64_t groups = 1;
-  if (n > 1) {  // scratch follows the partials
-    LaunchInfo li;
-    int64_t grid;
-    if ((rc = grid_for(logn, K_BWD, rows > 0 ? rows : 1, &li, &grid))) return rc;
-    p.scratch = p.ws + grid * li.gpc * 3 * (int64_t)n;
-  }
   if (rows == 0) {
     if (!accumulate) {
       cudaMemsetAsync(grad_a, 0, sizeof(float) * n, st);
@@ -966,11 +802,12 @@ int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, con
   if (n == 1) {
     acdc_n1_bwd_kernel<<<1, 256, 0, st>>>(p);
   } else {
-    if ((rc = run(K_BWD, p, n, st))) return rc;
     LaunchInfo li;
     int64_t grid;
-    if ((rc = grid_for(logn, K_BWD, rows, &li, &grid))) return rc;
+    if ((rc = sized(logn, K_BWD, rows, &li, &grid))) return rc;
     groups = grid * li.gpc;
+    p.scratch = p.ws + groups * 3 * (int64_t)n;  // scratch follows the partials
+    if ((rc = run(K_BWD, p, n, st))) return rc;
   }
   const int64_t total = 3LL * n;
   int blocks = (int)((total + 31) / 32);
@@ -980,7 +817,8 @@ int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, con
   return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
 }
 
-int acdc_dct2_f32(const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream) {
+static int transform(int kind, const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy,
+                     acdc_stream_t stream) {
   int rc = check_common(x, y, rows, n, ldx, ldy);
   if (rc) return rc;
   KParams p{};
@@ -994,24 +832,15 @@ int acdc_dct2_f32(const float* x, float* y, int64_t rows, int32_t n, int64_t ldx
     cudaError_t e = cudaMemcpy2DAsync(y, ldy * 4, x, ldx * 4, 4, rows, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
     return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
   }
-  return run(K_DCT2, p, n, (cudaStream_t)stream);
+  return run(kind, p, n, (cudaStream_t)stream);
+}
+
+int acdc_dct2_f32(const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream) {
+  return transform(K_DCT2, x, y, rows, n, ldx, ldy, stream);
 }
 
 int acdc_dct3_f32(const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream) {
-  int rc = check_common(x, y, rows, n, ldx, ldy);
-  if (rc) return rc;
-  KParams p{};
-  p.x = x;
-  p.y = y;
-  p.rows = rows;
-  p.ldx = ldx;
-  p.ldo = ldy;
-  if (n == 1) {
-    if (rows == 0) return ACDC_OK;
-    cudaError_t e = cudaMemcpy2DAsync(y, ldy * 4, x, ldx * 4, 4, rows, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
-    return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
-  }
-  return run(K_DCT3, p, n, (cudaStream_t)stream);
+  return transform(K_DCT3, x, y, rows, n, ldx, ldy, stream);
 }
 
 }  // extern "C"

@@ -24,6 +24,12 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#ifdef ACDC_NO_LB  // experiments: report the natural register demand
+#define ACDC_LB(G)
+#else
+#define ACDC_LB(G) __launch_bounds__(G::CTA, G::MINB)
+#endif
+
 namespace acdc {
 
 // ------------------------------------------------------------ complex helpers

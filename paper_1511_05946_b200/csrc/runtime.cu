@@ -1,0 +1,183 @@
+// Host runtime: twiddle tables, persistent-grid sizing, error state, and the
+// size-independent C-ABI entry points (acdc_abi_version, acdc_strerror, ...).
+#include "runtime.h"
+
+#include <cmath>
+#include <cstdio>
+#include <map>
+#include <mutex>
+#include <utility>
+#include <vector>
+
+namespace acdc {
+
+static std::mutex g_mu;
+static std::map<std::pair<int, int>, Tables> g_tables;
+static std::map<std::pair<int, const void*>, std::pair<int, int>> g_occ;  // (dev, fn) -> (blocks/SM, SMs)
+static thread_local char g_errbuf[256];
+static thread_local const char* g_last_error = "";
+
+int set_cuda_error(cudaError_t e) {
+  snprintf(g_errbuf, sizeof(g_errbuf), "CUDA error: %s", cudaGetErrorString(e));
+  g_last_error = g_errbuf;
+  return ACDC_E_CUDA;
+}
+
+int set_error(int code, const char* msg) {
+  snprintf(g_errbuf, sizeof(g_errbuf), "%s", msg);
+  g_last_error = g_errbuf;
+  return code;
+}
+
+int check_n(int32_t n, int* logn) {
+  if (n < 1 || (n & (n - 1)) != 0) {
+    snprintf(g_errbuf, sizeof(g_errbuf), "fast DCT requires a power-of-two size, got %d", n);
+    g_last_error = g_errbuf;
+    return ACDC_E_SIZE;
+  }
+  int l = 0;
+  while ((1 << l) < n) ++l;
+  if (l > 15) {
+    snprintf(g_errbuf, sizeof(g_errbuf), "size %d exceeds the on-chip limit 32768", n);
+    g_last_error = g_errbuf;
+    return ACDC_E_SIZE;
+  }
+  *logn = l;
+  return ACDC_OK;
+}
+
+// exp(-2 pi i m / M) in double, rounded once to fp32
+static float2 twiddle(long m, long M) {
+  const double pi = 3.14159265358979323846264338327950288;
+  m %= M;
+  const double th = 2.0 * pi * (double)m / (double)M;
+  return make_float2((float)std::cos(th), (float)-std::sin(th));
+}
+
+// Host mirror of Plan<LOGN> (radix 16 x small x 16 ...), fft_engine.cuh.
+static void host_plan(int logn, std::vector<int>& radix) {
+  radix.clear();
+  const int n = 1 << logn;
+  if (logn < 4) {
+    radix.push_back(n);
+    return;
+  }
+  const int a16 = logn / 4, rem = logn % 4;
+  const int np = a16 + (rem ? 1 : 0);
+  for (int p = 0; p < np; ++p) radix.push_back((rem && p == 1) ? (1 << rem) : 16);
+}
+
+int get_tables(int logn, Tables* out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return set_cuda_error(e);
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_pair(dev, logn);
+  auto it = g_tables.find(key);
+  if (it != g_tables.end()) {
+    *out = it->second;
+    return ACDC_OK;
+  }
+  const int n = 1 << logn;
+  std::vector<int> radix;
+  host_plan(logn, radix);
+  std::vector<float2> h;
+  long ns = radix[0];
+  for (size_t p = 1; p < radix.size(); ++p) {
+    const int r = radix[p];
+    for (int q = 1; q < r; ++q)
+      for (long k = 0; k < ns; ++k) h.push_back(twiddle((long)q * k, ns * r));
+    ns *= r;
+  }
+  const double pi = 3.14159265358979323846264338327950288;
+  for (int k = 0; k <= n / 2; ++k) {
+    const double s = (k == 0 ? std::sqrt(1.0 / n) : std::sqrt(2.0 / n)) * 0.5;
+    const double th = pi * (double)k / (2.0 * n);
+    h.push_back(make_float2((float)(s * std::cos(th)), (float)(-s * std::sin(th))));
+  }
+  Tables tb;
+  if ((e = cudaMalloc(&tb.tab, sizeof(float2) * h.size())) != cudaSuccess) return set_cuda_error(e);
+  if ((e = cudaMemcpy(tb.tab, h.data(), sizeof(float2) * h.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+    return set_cuda_error(e);
+  g_tables[key] = tb;
+  *out = tb;
+  return ACDC_OK;
+}
+
+int grid_for(const LaunchInfo& li, int64_t units, int64_t* grid) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return set_cuda_error(e);
+  std::pair<int, int> occ;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto key = std::make_pair(dev, li.fn);
+    auto it = g_occ.find(key);
+    if (it == g_occ.end()) {
+      if (li.smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(li.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, li.smem);
+        if (e != cudaSuccess) return set_cuda_error(e);
+      }
+      int bps = 0, sms = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, li.fn, li.cta, li.smem);
+      if (e != cudaSuccess) return set_cuda_error(e);
+      e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (e != cudaSuccess) return set_cuda_error(e);
+      if (bps < 1) return set_error(ACDC_E_CUDA, "kernel does not fit on an SM (registers / shared memory)");
+      occ = std::make_pair(bps, sms);
+      g_occ[key] = occ;
+    } else {
+      occ = it->second;
+    }
+  }
+  const int64_t need = (units + li.gpc - 1) / li.gpc;
+  const int64_t cap = (int64_t)occ.first * occ.second;
+  *grid = need < cap ? need : cap;
+  if (*grid < 1) *grid = 1;
+  return ACDC_OK;
+}
+
+int launch(const LaunchInfo& li, int64_t grid, void* params, cudaStream_t st) {
+  void* args[] = {params};
+  cudaError_t e = cudaLaunchKernel(li.fn, dim3((unsigned)grid), dim3(li.cta), args, li.smem, st);
+  if (e != cudaSuccess) return set_cuda_error(e);
+  return ACDC_OK;
+}
+
+const char* last_error() { return g_last_error; }
+
+}  // namespace acdc
+
+using namespace acdc;
+
+extern "C" {
+
+int acdc_abi_version(void) { return ACDC_ABI_VERSION; }
+
+const char* acdc_strerror(int code) {
+  const char* le = last_error();
+  switch (code) {
+    case ACDC_OK:
+      return "ok";
+    case ACDC_E_SIZE:
+      return le[0] ? le : "unsupported size";
+    case ACDC_E_CUDA:
+      return le[0] ? le : "CUDA error";
+    case ACDC_E_SHAPE:
+      return "invalid shape or leading dimension";
+    case ACDC_E_ALIGN:
+      return "misaligned pointer or leading dimension (n >= 256 needs 8-byte aligned rows)";
+    case ACDC_E_WS:
+      return "workspace too small";
+    case ACDC_E_NULL:
+      return "null pointer argument";
+    default:
+      return "unknown error";
+  }
+}
+
+const char* acdc_last_error(void) { return last_error(); }
+
+int acdc_max_n(void) { return 32768; }
+
+}  // extern "C"

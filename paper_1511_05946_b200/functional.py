@@ -16,7 +16,19 @@ import torch
 
 from . import _lib
 
-__all__ = ["acdc_forward", "acdc_backward", "dct", "idct", "AcdcFunction", "acdc", "prepare"]
+__all__ = [
+    "acdc_forward",
+    "acdc_backward",
+    "dct",
+    "idct",
+    "AcdcFunction",
+    "acdc",
+    "afdf_forward",
+    "afdf_backward",
+    "AfdfFunction",
+    "afdf",
+    "prepare",
+]
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -165,3 +177,89 @@ class AcdcFunction(torch.autograd.Function):
 def acdc(x, a, d, bias):
     """Differentiable ACDC layer: ``AcdcFunction.apply``."""
     return AcdcFunction.apply(x, a, d, bias)
+
+
+# ----------------------------------------------------------------- AFDF
+
+
+def _crows2d(x: torch.Tensor, n: int, name: str = "x") -> torch.Tensor:
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if x.dim() != 2 or x.shape[1] != n:
+        raise ValueError(f"{name} must have shape (batch, {n}), got {tuple(x.shape)}")
+    if x.dtype != torch.complex64:
+        x = x.to(torch.complex64)
+    return x.contiguous()
+
+
+def _cvec(v: torch.Tensor, n: int, dev, name: str) -> torch.Tensor:
+    if v.dim() != 1 or v.shape[0] != n:
+        raise ValueError(f"{name} must have shape ({n},), got {tuple(v.shape)}")
+    return v.to(device=dev, dtype=torch.complex64).contiguous()
+
+
+def afdf_forward(x: torch.Tensor, a: torch.Tensor, d: torch.Tensor, out=None) -> torch.Tensor:
+    """y = IFFT(d * FFT(a * x)) row-wise, complex64 (layers.py:199-204)."""
+    n = a.shape[0]
+    x = _crows2d(x, n)
+    a, d = _cvec(a, n, x.device, "a"), _cvec(d, n, x.device, "d")
+    y = torch.empty_like(x) if out is None else out
+    lib = _lib.load()
+    with torch.cuda.device(x.device):
+        _lib.check(lib.afdf_fwd_c64(_ptr(x), _ptr(y), _ptr(a), _ptr(d), x.shape[0], n, n, n, _stream(x)))
+    return y
+
+
+def afdf_backward(x, dy, a, d, grad_a, grad_d, accumulate: bool = True, out=None) -> torch.Tensor:
+    """dx and (accumulated) complex diagonal gradients dL/dRe + i dL/dIm
+    (layers.py:206-215).  grad_a / grad_d: complex64 (n,) CUDA tensors, in place."""
+    n = a.shape[0]
+    x = _crows2d(x, n)
+    dy = _crows2d(dy, n, "grad_y")
+    if dy.shape[0] != x.shape[0]:
+        raise ValueError(f"grad_y has {dy.shape[0]} rows, input had {x.shape[0]}")
+    dev = x.device
+    a, d = _cvec(a, n, dev, "a"), _cvec(d, n, dev, "d")
+    for g in (grad_a, grad_d):
+        if g.device != dev or g.dtype != torch.complex64 or not g.is_contiguous() or g.shape != (n,):
+            raise ValueError("gradient buffers must be contiguous complex64 (n,) tensors on the input device")
+    dx = torch.empty_like(x) if out is None else out
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        wsb = lib.afdf_bwd_workspace_bytes(x.shape[0], n)
+        if wsb == 0:
+            _lib.check(_lib.ACDC_E_SIZE if n > 16384 or n < 2 else _lib.ACDC_E_CUDA)
+        ws = torch.empty((wsb + 3) // 4, dtype=torch.float32, device=dev)
+        _lib.check(
+            lib.afdf_bwd_c64(
+                _ptr(x), _ptr(dy), _ptr(dx), _ptr(a), _ptr(d), _ptr(grad_a), _ptr(grad_d), 1 if accumulate else 0,
+                _ptr(ws), wsb, x.shape[0], n, n, n, n, _stream(x),
+            )
+        )
+    return dx
+
+
+class AfdfFunction(torch.autograd.Function):
+    """Autograd wrapper for the complex AFDF layer.  The kernels return
+    dL/dRe + i dL/dIm, which is what torch's complex autograd propagates
+    (conjugate Wirtinger convention)."""
+
+    @staticmethod
+    def forward(ctx, x, a, d):
+        y = afdf_forward(x, a, d)
+        ctx.save_for_backward(x, a, d)
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, a, d = ctx.saved_tensors
+        n = a.shape[0]
+        ga = torch.empty(n, dtype=torch.complex64, device=x.device)
+        gd = torch.empty_like(ga)
+        dx = afdf_backward(x, gy, a, d, ga, gd, accumulate=False)
+        return dx, ga, gd
+
+
+def afdf(x, a, d):
+    """Differentiable AFDF layer: ``AfdfFunction.apply``."""
+    return AfdfFunction.apply(x, a, d)

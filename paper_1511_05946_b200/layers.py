@@ -29,11 +29,13 @@ __all__ = [
     "Param",
     "Layer",
     "AcdcLayer",
+    "AfdfLayer",
     "ReluLayer",
     "PermutationLayer",
     "DenseLayer",
     "Cascade",
     "acdc_cascade",
+    "afdf_cascade",
     "count_params",
 ]
 
@@ -173,6 +175,63 @@ class AcdcLayer(Layer):
         if gy.shape[0] != x.shape[0]:
             raise ValueError(f"grad_y has {gy.shape[0]} rows, forward input had {x.shape[0]}")
         dx = F.acdc_backward(x, gy, self.a, self.d, self.grad_a, self.grad_d, self.grad_bias_d, accumulate=True)
+        return self._out(dx, host)
+
+
+class AfdfLayer(Layer):
+    """Complex diagonals around the FFT pair, no bias (layers.py:159-215).
+
+    Gradients are dL/dRe + i dL/dIm (layers.py:162-164).  ``fix_a`` removes
+    ``a`` from ``params()`` (its gradient is still computed, layers.py:192-194,
+    214); ``param_count`` stays 4N (layers.py:196-197).
+    """
+
+    linear = True
+    complex_domain = True
+
+    def __init__(self, n, backend="auto", fix_a=False, device=None):
+        if not _is_pow2(n):
+            raise ValueError(f"FFT size must be a power of two, got {n}")
+        self.n_in = self.n_out = n
+        self.backend = backend
+        self.fix_a = fix_a
+        self.device = _device(device)
+        kw = dict(dtype=torch.complex64, device=self.device)
+        self.a = torch.ones(n, **kw)
+        self.d = torch.ones(n, **kw)
+        self.grad_a = torch.zeros(n, **kw)
+        self.grad_d = torch.zeros(n, **kw)
+        self._params = [Param("a", self.a, self.grad_a), Param("d", self.d, self.grad_d)]
+        self._cache = None
+        F.prepare(n, self.device)
+
+    @property
+    def n(self):
+        return self.n_in
+
+    def params(self):
+        return self._params[1:] if self.fix_a else self._params
+
+    def param_count(self):
+        return 4 * self.n_in
+
+    def _out(self, y, host):
+        if not host:
+            return y
+        return y.detach().to("cpu", dtype=torch.complex128).numpy()
+
+    def forward(self, x):
+        x, host = self._check_input(x, torch.complex64)
+        y = F.afdf_forward(x, self.a, self.d)
+        self._cache = x
+        return self._out(y, host)
+
+    def backward(self, grad_y, retain_cache=False):
+        x = self._take_cache(retain_cache)
+        gy, host = self._check_input(grad_y, torch.complex64)
+        if gy.shape[0] != x.shape[0]:
+            raise ValueError(f"grad_y has {gy.shape[0]} rows, forward input had {x.shape[0]}")
+        dx = F.afdf_backward(x, gy, self.a, self.d, self.grad_a, self.grad_d, accumulate=True)
         return self._out(dx, host)
 
 
@@ -333,6 +392,11 @@ class Cascade:
 def acdc_cascade(n, depth, dct_mode="fast", backend="auto", device=None):
     """``depth`` identity-configured ACDC layers of size n (layers.py:360-362)."""
     return Cascade([AcdcLayer(n, dct_mode=dct_mode, backend=backend, device=device) for _ in range(depth)])
+
+
+def afdf_cascade(n, depth, backend="auto", device=None):
+    """``depth`` AFDF layers; the first signal diagonal is fixed (layers.py:365-370)."""
+    return Cascade([AfdfLayer(n, backend=backend, fix_a=(i == 0), device=device) for i in range(depth)])
 
 
 def count_params(obj):

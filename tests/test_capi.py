@@ -13,7 +13,7 @@ HEADER = os.path.join(ROOT, "include", "acdc_b200.h")
 
 def _declared():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(acdc_[a-z0-9_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b((?:acdc|afdf|cascade)_[a-z0-9_]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")
