@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--mode", default="auto", choices=["auto", "recompute", "h2cache"],
+                    help="recompute h2 in the backward (PAPER.md:275) or cache it from the forward "
+                         "(layers.py:145); auto times both and reports the faster")
     return ap.parse_args()
 
 
@@ -246,47 +249,68 @@ def run_ours(args):
     dx = torch.empty_like(x)
     F.prepare(n, dev)
     stream = torch.cuda.current_stream()
+    cache = F.new_h2cache(B, n, dev) if F.h2cache_supported(n) else None
 
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    def timed(mode):
+        """W warm-up + exactly K timed steps of one mode; per-kernel CUDA events."""
+        hc = cache if mode == "h2cache" else None
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
 
-    def step(i=None):
-        e = ev[i] if i is not None else None
-        if e: e[0].record(stream)
-        F.acdc_forward(x, a, d, bias, out=y)
-        if e: e[1].record(stream)
-        F.acdc_backward(x, dy, a, d, grads[0], grads[1], grads[2], accumulate=False, out=dx)
-        if e: e[2].record(stream)
-        if world > 1:
-            dist.all_reduce(grads)
-        if e: e[3].record(stream)
+        def step(i=None):
+            e = ev[i] if i is not None else None
+            if e: e[0].record(stream)
+            F.acdc_forward(x, a, d, bias, out=y, h2cache=hc)
+            if e: e[1].record(stream)
+            F.acdc_backward(x, dy, a, d, grads[0], grads[1], grads[2], accumulate=False, out=dx, h2cache=hc)
+            if e: e[2].record(stream)
+            if world > 1:
+                dist.all_reduce(grads)
+            if e: e[3].record(stream)
 
-    for _ in range(max(args.warmup, 3)):
-        step()
-    barrier(world)
-    sampler = ClockSampler(local)
-    sampler.start()
-    time.sleep(0.15)
-    barrier(world)
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for i in range(args.steps):
-        step(i)
-    t1.record(stream)
-    barrier(world)
-    clocks = sampler.stop()
-    elapsed_ms = t0.elapsed_time(t1)
-    fwd_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps
-    bwd_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps
-    ar_ms = sum(e[2].elapsed_time(e[3]) for e in ev) / args.steps
-    max_ms = max_over_ranks(elapsed_ms, world)
+        for _ in range(max(args.warmup, 3)):
+            step()
+        barrier(world)
+        sampler = ClockSampler(local)
+        sampler.start()
+        time.sleep(0.15)
+        barrier(world)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        t1.record(stream)
+        barrier(world)
+        clocks = sampler.stop()
+        max_ms = max_over_ranks(t0.elapsed_time(t1), world)
+        return {
+            "mode": mode,
+            "max_ms": max_ms,
+            "fwd_ms": sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps,
+            "bwd_ms": sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps,
+            "ar_ms": sum(e[2].elapsed_time(e[3]) for e in ev) / args.steps,
+            "clocks": clocks,
+            "value": world * B * args.steps / (max_ms / 1e3),
+        }
+
+    modes = ["recompute"] if (cache is None or args.mode == "recompute") else (
+        ["h2cache"] if args.mode == "h2cache" else ["recompute", "h2cache"])
+    runs = [timed(m) for m in modes]
+    best = max(runs, key=lambda r: r["value"])
+    other = [r for r in runs if r is not best]
+    fwd_ms, bwd_ms, ar_ms, clocks = best["fwd_ms"], best["bwd_ms"], best["ar_ms"], best["clocks"]
+    max_ms = best["max_ms"]
     ms_per_step = max_ms / args.steps
-    value = world * B * args.steps / (max_ms / 1e3)
+    value = best["value"]
+    # bytes per row moved by each kernel in the chosen mode (h2 cache adds 4N out + 4N in)
+    cache_b = 4 * n if best["mode"] == "h2cache" else 0
+    bytes_fwd, bytes_bwd = 8 * n + cache_b, 12 * n + cache_b
 
     # e2e through the public API with host buffers (pinned), copies in the timed region
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_measure(F, n, B, a, d, bias, dev, world, steps=max(3, min(args.steps, 10)))
+        e2e = e2e_measure(F, n, B, a, d, bias, dev, world, steps=max(3, min(args.steps, 10)),
+                          h2cache=cache if best["mode"] == "h2cache" else None)
 
     dense = None
     if not args.no_dense and rank == 0:
@@ -297,9 +321,9 @@ def run_ours(args):
         hbm, src = peaks()
         # dominant kernel = the longer of fwd / bwd (bwd: acdc_bwd_kernel + grad reduce)
         if bwd_ms >= fwd_ms:
-            kname, kms, kbytes = "acdc_bwd_kernel(+grad_reduce)", bwd_ms, BYTES_BWD * n // N_FEAT * B
+            kname, kms, kbytes = "acdc_bwd_kernel(+grad_reduce)", bwd_ms, bytes_bwd * B
         else:
-            kname, kms, kbytes = "acdc_fwd_kernel", fwd_ms, BYTES_FWD * n // N_FEAT * B
+            kname, kms, kbytes = "acdc_fwd_kernel", fwd_ms, bytes_fwd * B
         achieved = kbytes / (kms / 1e3) / 1e9
         step_bytes = (BYTES_FWD + BYTES_BWD) * n // N_FEAT * B
         step_gbs = step_bytes / ((fwd_ms + bwd_ms) / 1e3) / 1e9
@@ -343,8 +367,11 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": kbytes,
                 "avg_launch_ms": kms,
             },
+            "mode": best["mode"],
+            "other_modes": [{k: r[k] for k in ("mode", "value", "fwd_ms", "bwd_ms")} for r in other],
             "roofline_step": {
                 "bytes_per_row": (BYTES_FWD + BYTES_BWD) * n // N_FEAT,
+                "bytes_moved_per_row": bytes_fwd + bytes_bwd,
                 "achieved_gbs": step_gbs,
                 "frac": step_gbs / hbm,
                 "fwd_ms": fwd_ms,
@@ -352,7 +379,7 @@ def run_ours(args):
                 "allreduce_ms": ar_ms,
             },
             "clocks": clocks,
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": 3 * args.steps,  # fwd + bwd + grad reduce per step (this arm's timed region)
             "e2e": e2e,
             "dense_cublas": dense,
         }
@@ -366,7 +393,7 @@ def run_ours(args):
     return out
 
 
-def e2e_measure(F, n, B, a, d, bias, dev, world, steps):
+def e2e_measure(F, n, B, a, d, bias, dev, world, steps, h2cache=None):
     """Rows/s through the public API with pinned host buffers: H2D x, dy;
     forward; backward; D2H dx and grads — all inside the timed region."""
     import torch
@@ -383,8 +410,8 @@ def e2e_measure(F, n, B, a, d, bias, dev, world, steps):
     def step():
         xd.copy_(xh, non_blocking=True)
         dyd.copy_(dyh, non_blocking=True)
-        F.acdc_forward(xd, a, d, bias)
-        dx = F.acdc_backward(xd, dyd, a, d, grads[0], grads[1], grads[2], accumulate=False)
+        F.acdc_forward(xd, a, d, bias, h2cache=h2cache)
+        dx = F.acdc_backward(xd, dyd, a, d, grads[0], grads[1], grads[2], accumulate=False, h2cache=h2cache)
         if world > 1:
             dist.all_reduce(grads)
         dxh.copy_(dx, non_blocking=True)

@@ -80,6 +80,20 @@ int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, con
                  float* grad_d, float* grad_bias, int accumulate, void* ws, size_t ws_bytes, int64_t rows,
                  int32_t n, int64_t ldx, int64_t ldy, int64_t lddx, acdc_stream_t stream);
 
+/* h2-cache variant (the reference caches h2 = C2(a*x) in forward, layers.py:145).
+ * acdc_fwd_cache_f32 also writes h2 into `h2cache` (acdc_h2cache_bytes(rows, n)
+ * bytes, opaque layout); acdc_bwd_cached_f32 reads it instead of recomputing
+ * C2(a*x), trading 8n bytes/row of HBM traffic for one of the backward's three
+ * transforms.  Same results as the pair above.  256 <= n <= 16384 (bytes() == 0
+ * otherwise). */
+size_t acdc_h2cache_bytes(int64_t rows, int32_t n);
+int acdc_fwd_cache_f32(const float* x, float* y, const float* a, const float* d, const float* bias, float* h2cache,
+                       int64_t rows, int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream);
+int acdc_bwd_cached_f32(const float* x, const float* dy, float* dx, const float* a, const float* d,
+                        const float* h2cache, float* grad_a, float* grad_d, float* grad_bias, int accumulate, void* ws,
+                        size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, int64_t lddx,
+                        acdc_stream_t stream);
+
 /* Row-wise orthonormal DCT-II / DCT-III (the reference dct / idct). */
 int acdc_dct2_f32(const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream);
 int acdc_dct3_f32(const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream);

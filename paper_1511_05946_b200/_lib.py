@@ -41,6 +41,12 @@ SIGNATURES = {
         ctypes.c_int,
         [_P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _I64, _I32, _I64, _I64, _I64, _P],
     ),
+    "acdc_h2cache_bytes": (ctypes.c_size_t, [_I64, _I32]),
+    "acdc_fwd_cache_f32": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I32, _I64, _I64, _P]),
+    "acdc_bwd_cached_f32": (
+        ctypes.c_int,
+        [_P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _I64, _I32, _I64, _I64, _I64, _P],
+    ),
     "acdc_dct2_f32": (ctypes.c_int, [_P, _P, _I64, _I32, _I64, _I64, _P]),
     "acdc_dct3_f32": (ctypes.c_int, [_P, _P, _I64, _I32, _I64, _I64, _P]),
     "afdf_fwd_c64": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I32, _I64, _I64, _P]),

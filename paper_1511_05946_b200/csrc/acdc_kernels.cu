@@ -21,7 +21,7 @@
 #include <tuple>
 #include <vector>
 
-#include "dct_pair.cuh"
+#include "kernel_common.cuh"
 #include "runtime.h"
 
 namespace acdc {
@@ -35,32 +35,13 @@ struct KParams {
   const float* bias;
   float* ws;          // bwd partials [groups][3][N]
   float* scratch;     // bwd stash when it does not fit in smem [groups][STASH*T]
+  float* h2c;         // h2 cache [row pairs][2N] in thread-native layout (H2C kernels)
   const float2* tab;  // [pass twiddles | c'_k]
   int64_t rows;
   int64_t ldx, ldy, ldo;
 };
 
 // ---------------------------------------------------------------- helpers
-
-// Bulk prefetch of one row into L2 (TMA engine; no registers, no smem).
-__device__ __forceinline__ void prefetch_row_l2(const float* row, int n) {
-  uintptr_t a = reinterpret_cast<uintptr_t>(row);
-  uintptr_t lo = a & ~uintptr_t(15);
-  uintptr_t hi = (a + uintptr_t(n) * 4 + 15) & ~uintptr_t(15);
-  for (uintptr_t p = lo; p < hi; p += 32768) {
-    uint32_t bytes = (uint32_t)((hi - p) < 32768 ? (hi - p) : 32768);
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-  }
-}
-
-// Plain (coherent) global load: unlike ld.global.nc it is ordered by the group
-// barriers, so ptxas cannot hoist it to the top of the row iteration where it
-// would pin a register across every FFT pass.
-__device__ __forceinline__ float ld_plain(const float* p) {
-  float r;
-  asm volatile("ld.global.f32 %0, [%1];" : "=f"(r) : "l"(p) : "memory");
-  return r;
-}
 
 // Row pointers of the Makhoul-reordered first/last pass slots of thread t.
 template <class G>
@@ -133,42 +114,13 @@ __device__ __forceinline__ void packed_dct3(float2 (&Y)[G::E], float2 (&v)[G::E]
   fft_passes<G>(v, xb, gs, tw, t);
 }
 
-template <class G>
-struct GroupCtx {
-  int grp, t;
-  int64_t gid, gstride;
-};
-
-template <class G>
-__device__ __forceinline__ GroupCtx<G> group_ctx() {
-  GroupCtx<G> c;
-  c.grp = threadIdx.x / G::T;
-  c.t = threadIdx.x % G::T;
-  c.gid = (int64_t)blockIdx.x * G::GPC + c.grp;
-  c.gstride = (int64_t)gridDim.x * G::GPC;
-  return c;
-}
-
-// Stage the pass-twiddle / post-twiddle tables in shared memory (whole CTA)
-// when the plan has room; return the table pointers the kernel should use.
-template <class G>
-__device__ __forceinline__ void stage_tables(const KParams& p, float* smem, const float2*& tw, const float2*& cp) {
-  constexpr int TOT = G::TW_ENTRIES + G::CP_ENTRIES;
-  if constexpr (G::TW_SMEM) {
-    float2* st = reinterpret_cast<float2*>(smem);
-    for (int i = threadIdx.x; i < TOT; i += blockDim.x) st[i] = p.tab[i];
-    __syncthreads();
-    tw = st;
-  } else {
-    tw = p.tab;
-  }
-  cp = tw + G::TW_ENTRIES;
-}
-
 // ---------------------------------------------------------------- kernels
 
 // y = C3(d * C2(a * x) + bias)          (layers.py:141-146)
-template <int LOGN>
+// H2C: also store h2 = C2(a * x) (the reference's cache, layers.py:145) in a
+// thread-native layout: row pair rp, slot i, thread t at h2c[rp*2N + 2*(i*T + t)]
+// as (rowA, rowB).  Only the fast-pairing sizes (N >= 256) support it.
+template <int LOGN, bool H2C>
 __global__ void ACDC_LB(Geo<LOGN>) acdc_fwd_kernel(KParams p) {
   using G = Geo<LOGN>;
   constexpr int E = G::E;
@@ -179,7 +131,7 @@ __global__ void ACDC_LB(Geo<LOGN>) acdc_fwd_kernel(KParams p) {
   GroupSync<G> gs(c.grp);
   Xbuf<G> xb{smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS, 0};
   const float2 *tw, *cp;
-  stage_tables<G>(p, smem_f, tw, cp);
+  stage_tables<G>(p.tab, smem_f, tw, cp);
   const int64_t npairs = (p.rows + 1) >> 1;
   if constexpr (G::FP) {
     const FastMap<G> fm(t, gs.mask);
@@ -203,6 +155,11 @@ __global__ void ACDC_LB(Geo<LOGN>) acdc_fwd_kernel(KParams p) {
           const float2 cs = tab_load<G>(fm.plo(cp, s), 0);
           float2 xl, xh;
           dct2_post(v[s], w[s], cs, fm.special(s), chi, xl, xh);
+          if constexpr (H2C) {
+            float2* hc = reinterpret_cast<float2*>(p.h2c + rp * 2 * G::N) + t;
+            hc[(2 * s) * G::T] = xl;
+            hc[(2 * s + 1) * G::T] = xh;
+          }
           const float dl = ld_plain(fm.plo(p.d, s)), bl = ld_plain(fm.plo(p.bias, s));
           const float dh = ld_plain(fm.phi(p.d, s)), bh = ld_plain(fm.phi(p.bias, s));
           xl = make_float2(fmaf(xl.x, dl, bl), fmaf(xl.y, dl, bl));
@@ -270,7 +227,9 @@ __global__ void ACDC_LB(Geo<LOGN>) acdc_fwd_kernel(KParams p) {
 template <int LOGN>
 using GeoBwd = Geo<LOGN, 3 * Geo<LOGN>::E>;  // stash: g3 (E float2) + grad_a (E floats)
 
-template <int LOGN>
+// H2C: read h2 from the forward's cache instead of recomputing C2(a * x);
+// the backward then runs 2 packed FFTs instead of 3 and needs no g3 stash.
+template <int LOGN, bool H2C>
 __global__ void ACDC_LB(GeoBwd<LOGN>) acdc_bwd_kernel(KParams p) {
   using G = GeoBwd<LOGN>;
   constexpr int E = G::E;
@@ -287,7 +246,7 @@ __global__ void ACDC_LB(GeoBwd<LOGN>) acdc_bwd_kernel(KParams p) {
   float2* st_g3 = reinterpret_cast<float2*>(sbase) + t;  // [E][T]
   float* st_ga = sbase + 2 * E * T + t;                  // [E][T]
   const float2 *tw, *cp;
-  stage_tables<G>(p, smem_f, tw, cp);
+  stage_tables<G>(p.tab, smem_f, tw, cp);
   float acc_d[E], acc_b[E];
 #pragma unroll
   for (int i = 0; i < E; ++i) {
@@ -320,6 +279,27 @@ __global__ void ACDC_LB(GeoBwd<LOGN>) acdc_bwd_kernel(KParams p) {
       // g3 = C2(dy): grad_bias partial, stash
       fp_load<G, false>(v, p.dy + ra * p.ldy, hasb ? p.dy + (ra + 1) * p.ldy : nullptr, nullptr, fm);
       fft_passes<G, 0>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
+      if constexpr (H2C) {
+        // g3 and the cached h2 in one slot pass: grad_bias, grad_d, Y = d * g3
+        float2 w[8], gl[8], gh[8];
+        fp_partner<G>(v, w, fm);
+        const float2* hc = reinterpret_cast<const float2*>(p.h2c + rp * 2 * G::N) + t;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          const float2 cs = tab_load<G>(fm.plo(cp, s), 0);
+          float2 g3l, g3h;
+          dct2_post(v[s], w[s], cs, fm.special(s), chi, g3l, g3h);
+          acc_b[2 * s] += g3l.x + g3l.y;
+          acc_b[2 * s + 1] += g3h.x + g3h.y;
+          const float2 hl = __ldcs(hc + (2 * s) * G::T), hh = __ldcs(hc + (2 * s + 1) * G::T);
+          acc_d[2 * s] = fmaf(hl.x, g3l.x, fmaf(hl.y, g3l.y, acc_d[2 * s]));
+          acc_d[2 * s + 1] = fmaf(hh.x, g3h.x, fmaf(hh.y, g3h.y, acc_d[2 * s + 1]));
+          const float dl = ld_plain(fm.plo(p.d, s)), dh = ld_plain(fm.phi(p.d, s));
+          dct3_pre(make_float2(g3l.x * dl, g3l.y * dl), make_float2(g3h.x * dh, g3h.y * dh), cs, fm.special(s), chi,
+                   gl[s], gh[s]);
+        }
+        fp_scatter<G>(gl, gh, v, fm);
+      } else {
       {
         float2 w[8];
         fp_partner<G>(v, w, fm);
@@ -353,6 +333,7 @@ __global__ void ACDC_LB(GeoBwd<LOGN>) acdc_bwd_kernel(KParams p) {
         }
         fp_scatter<G>(gl, gh, v, fm);
       }
+      }  // !H2C
       // g1 = C3(d * g3); dx = a * g1; grad_a partial += x * g1
       fft_passes<G, 0>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
       float2 ga[8], gb[8];
@@ -491,7 +472,7 @@ __global__ void ACDC_LB(Geo<LOGN>) acdc_dct2_kernel(KParams p) {
   GroupSync<G> gs(c.grp);
   Xbuf<G> xb{smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS, 0};
   const float2 *tw, *cp;
-  stage_tables<G>(p, smem_f, tw, cp);
+  stage_tables<G>(p.tab, smem_f, tw, cp);
   const Slots<G> sl(t);
   const int64_t npairs = (p.rows + 1) >> 1;
   for (int64_t rp = c.gid; rp < npairs; rp += c.gstride) {
@@ -526,7 +507,7 @@ __global__ void ACDC_LB(Geo<LOGN>) acdc_dct3_kernel(KParams p) {
   GroupSync<G> gs(c.grp);
   Xbuf<G> xb{smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS, 0};
   const float2 *tw, *cp;
-  stage_tables<G>(p, smem_f, tw, cp);
+  stage_tables<G>(p.tab, smem_f, tw, cp);
   const Slots<G> sl(t);
   const int64_t npairs = (p.rows + 1) >> 1;
   for (int64_t rp = c.gid; rp < npairs; rp += c.gstride) {
@@ -624,21 +605,25 @@ __global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __re
 
 // ---------------------------------------------------------------- host side
 
-enum Kind { K_FWD = 0, K_BWD = 1, K_DCT2 = 2, K_DCT3 = 3 };
+enum Kind { K_FWD = 0, K_BWD = 1, K_DCT2 = 2, K_DCT3 = 3, K_FWD_H2 = 4, K_BWD_H2 = 5 };
 
 template <int LOGN>
 static LaunchInfo info_for(int kind) {
   using G = Geo<LOGN>;
   using GB = GeoBwd<LOGN>;
   LaunchInfo li;
-  li.fn = kind == K_FWD    ? (const void*)acdc_fwd_kernel<LOGN>
-          : kind == K_BWD  ? (const void*)acdc_bwd_kernel<LOGN>
-          : kind == K_DCT2 ? (const void*)acdc_dct2_kernel<LOGN>
-                           : (const void*)acdc_dct3_kernel<LOGN>;
+  constexpr bool FP = G::FP;  // the h2 cache exists only on the fast-pairing path
+  li.fn = kind == K_FWD      ? (const void*)acdc_fwd_kernel<LOGN, false>
+          : kind == K_BWD    ? (const void*)acdc_bwd_kernel<LOGN, false>
+          : kind == K_DCT2   ? (const void*)acdc_dct2_kernel<LOGN>
+          : kind == K_DCT3   ? (const void*)acdc_dct3_kernel<LOGN>
+          : kind == K_FWD_H2 ? (FP ? (const void*)acdc_fwd_kernel<LOGN, FP> : nullptr)
+                             : (FP ? (const void*)acdc_bwd_kernel<LOGN, FP> : nullptr);
+  const bool bwd = kind == K_BWD || kind == K_BWD_H2;
   li.cta = G::CTA;
   li.gpc = G::GPC;
-  li.scratch = kind == K_BWD ? GB::GSCRATCH_FLOATS : 0;
-  li.smem = kind == K_BWD ? GB::SMEM_BYTES : G::SMEM_BYTES;
+  li.scratch = bwd ? GB::GSCRATCH_FLOATS : 0;
+  li.smem = bwd ? GB::SMEM_BYTES : G::SMEM_BYTES;
   return li;
 }
 
@@ -676,6 +661,7 @@ static int launch_info(int logn, int kind, LaunchInfo* li) {
 static int sized(int logn, int kind, int64_t rows, LaunchInfo* li, int64_t* grid) {
   int rc = launch_info(logn, kind, li);
   if (rc) return rc;
+  if (!li->fn) return set_error(ACDC_E_SIZE, "the h2 cache needs n >= 256 and n <= 16384");
   return grid_for(*li, (rows + 1) / 2, grid);
 }
 
@@ -726,11 +712,12 @@ static int check_common(const void* x, const void* y, int64_t rows, int32_t n, i
   return ACDC_OK;
 }
 
-int acdc_fwd_f32(const float* x, float* y, const float* a, const float* d, const float* bias, int64_t rows, int32_t n,
-                 int64_t ldx, int64_t ldy, acdc_stream_t stream) {
+static int fwd_impl(int kind, const float* x, float* y, const float* a, const float* d, const float* bias, float* h2c,
+                    int64_t rows, int32_t n, int64_t ldx, int64_t ldy, cudaStream_t st) {
   int rc = check_common(x, y, rows, n, ldx, ldy);
   if (rc) return rc;
   if (!a || !d || !bias) return ACDC_E_NULL;
+  if (kind == K_FWD_H2 && rows > 0 && !h2c) return ACDC_E_NULL;
   if (!pair_aligned(n, x, ldx) || !pair_aligned(n, y, ldy) || !pair_aligned(n, a, 0)) return ACDC_E_ALIGN;
   KParams p{};
   p.x = x;
@@ -738,11 +725,12 @@ int acdc_fwd_f32(const float* x, float* y, const float* a, const float* d, const
   p.a = a;
   p.d = d;
   p.bias = bias;
+  p.h2c = h2c;
   p.rows = rows;
   p.ldx = ldx;
   p.ldo = ldy;
-  cudaStream_t st = (cudaStream_t)stream;
   if (n == 1) {
+    if (kind != K_FWD) return set_error(ACDC_E_SIZE, "the h2 cache needs n >= 256 and n <= 16384");
     if (rows == 0) return ACDC_OK;
     int blocks = (int)((rows + 255) / 256);
     if (blocks > 1024) blocks = 1024;
@@ -750,7 +738,23 @@ int acdc_fwd_f32(const float* x, float* y, const float* a, const float* d, const
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
   }
-  return run(K_FWD, p, n, st);
+  return run(kind, p, n, st);
+}
+
+int acdc_fwd_f32(const float* x, float* y, const float* a, const float* d, const float* bias, int64_t rows, int32_t n,
+                 int64_t ldx, int64_t ldy, acdc_stream_t stream) {
+  return fwd_impl(K_FWD, x, y, a, d, bias, nullptr, rows, n, ldx, ldy, (cudaStream_t)stream);
+}
+
+size_t acdc_h2cache_bytes(int64_t rows, int32_t n) {
+  if (n < 256 || n > 16384 || (n & (n - 1)) != 0 || rows < 0) return 0;
+  return (size_t)((rows + 1) / 2) * 2 * (size_t)n * sizeof(float);
+}
+
+int acdc_fwd_cache_f32(const float* x, float* y, const float* a, const float* d, const float* bias, float* h2cache,
+                       int64_t rows, int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream) {
+  if (acdc_h2cache_bytes(rows, n) == 0) return set_error(ACDC_E_SIZE, "the h2 cache needs n >= 256 and n <= 16384");
+  return fwd_impl(K_FWD_H2, x, y, a, d, bias, h2cache, rows, n, ldx, ldy, (cudaStream_t)stream);
 }
 
 size_t acdc_bwd_workspace_bytes(int64_t rows, int32_t n) {
@@ -763,9 +767,11 @@ size_t acdc_bwd_workspace_bytes(int64_t rows, int32_t n) {
   return (size_t)grid * li.gpc * (3 * (size_t)n + (size_t)li.scratch) * sizeof(float);
 }
 
-int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, const float* d, float* grad_a,
-                 float* grad_d, float* grad_bias, int accumulate, void* ws, size_t ws_bytes, int64_t rows, int32_t n,
-                 int64_t ldx, int64_t ldy, int64_t lddx, acdc_stream_t stream) {
+static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const float* a, const float* d,
+                    const float* h2c, float* grad_a, float* grad_d, float* grad_bias, int accumulate, void* ws,
+                    size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, int64_t lddx,
+                    acdc_stream_t stream) {
+  if (kind == K_BWD_H2 && rows > 0 && !h2c) return ACDC_E_NULL;
   int rc = check_common(x, dx, rows, n, ldx, lddx);
   if (rc) return rc;
   if (ldy < n) return ACDC_E_SHAPE;
@@ -785,6 +791,7 @@ int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, con
   p.a = a;
   p.d = d;
   p.ws = (float*)ws;
+  p.h2c = const_cast<float*>(h2c);
   p.rows = rows;
   p.ldx = ldx;
   p.ldy = ldy;
@@ -804,10 +811,10 @@ int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, con
   } else {
     LaunchInfo li;
     int64_t grid;
-    if ((rc = sized(logn, K_BWD, rows, &li, &grid))) return rc;
+    if ((rc = sized(logn, kind, rows, &li, &grid))) return rc;
     groups = grid * li.gpc;
     p.scratch = p.ws + groups * 3 * (int64_t)n;  // scratch follows the partials
-    if ((rc = run(K_BWD, p, n, st))) return rc;
+    if ((rc = run(kind, p, n, st))) return rc;
   }
   const int64_t total = 3LL * n;
   int blocks = (int)((total + 31) / 32);
@@ -815,6 +822,22 @@ int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, con
                                                   accumulate);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
+}
+
+int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, const float* d, float* grad_a,
+                 float* grad_d, float* grad_bias, int accumulate, void* ws, size_t ws_bytes, int64_t rows, int32_t n,
+                 int64_t ldx, int64_t ldy, int64_t lddx, acdc_stream_t stream) {
+  return bwd_impl(K_BWD, x, dy, dx, a, d, nullptr, grad_a, grad_d, grad_bias, accumulate, ws, ws_bytes, rows, n, ldx,
+                  ldy, lddx, stream);
+}
+
+int acdc_bwd_cached_f32(const float* x, const float* dy, float* dx, const float* a, const float* d,
+                        const float* h2cache, float* grad_a, float* grad_d, float* grad_bias, int accumulate, void* ws,
+                        size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, int64_t lddx,
+                        acdc_stream_t stream) {
+  if (acdc_h2cache_bytes(rows, n) == 0) return set_error(ACDC_E_SIZE, "the h2 cache needs n >= 256 and n <= 16384");
+  return bwd_impl(K_BWD_H2, x, dy, dx, a, d, h2cache, grad_a, grad_d, grad_bias, accumulate, ws, ws_bytes, rows, n,
+                  ldx, ldy, lddx, stream);
 }
 
 static int transform(int kind, const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy,

@@ -28,6 +28,8 @@ __all__ = [
     "AfdfFunction",
     "afdf",
     "prepare",
+    "h2cache_supported",
+    "new_h2cache",
 ]
 
 
@@ -69,8 +71,26 @@ def prepare(n: int, device=None) -> None:
         _lib.check(_lib.load().acdc_prepare(int(n)))
 
 
-def acdc_forward(x: torch.Tensor, a: torch.Tensor, d: torch.Tensor, bias: torch.Tensor, out=None) -> torch.Tensor:
-    """y = C3(d * C2(a * x) + bias) row-wise (layers.py:141-146)."""
+def h2cache_supported(n: int) -> bool:
+    """Sizes whose kernels can cache h2 = C2(a*x) between forward and backward."""
+    return 256 <= n <= 16384 and (n & (n - 1)) == 0
+
+
+def new_h2cache(rows: int, n: int, device) -> torch.Tensor:
+    """Buffer for the h2 cache of ``rows`` rows (opaque, kernel-native layout)."""
+    nbytes = _lib.load().acdc_h2cache_bytes(rows, n)
+    if nbytes == 0:
+        raise ValueError(f"the h2 cache needs 256 <= n <= 16384, got {n}")
+    return torch.empty(nbytes // 4, dtype=torch.float32, device=device)
+
+
+def acdc_forward(x: torch.Tensor, a: torch.Tensor, d: torch.Tensor, bias: torch.Tensor, out=None,
+                 h2cache: torch.Tensor | None = None) -> torch.Tensor:
+    """y = C3(d * C2(a * x) + bias) row-wise (layers.py:141-146).
+
+    With ``h2cache`` (from :func:`new_h2cache`) the kernel also stores
+    h2 = C2(a * x) for :func:`acdc_backward`, like the reference's cache
+    (layers.py:145)."""
     n = a.shape[0]
     x = _rows2d(x, n)
     dev = x.device
@@ -78,10 +98,13 @@ def acdc_forward(x: torch.Tensor, a: torch.Tensor, d: torch.Tensor, bias: torch.
     y = torch.empty_like(x, memory_format=torch.contiguous_format) if out is None else out
     lib = _lib.load()
     with torch.cuda.device(dev):
-        _lib.check(
-            lib.acdc_fwd_f32(_ptr(x), _ptr(y), _ptr(a), _ptr(d), _ptr(bias), x.shape[0], n, _ld(x, n), _ld(y, n),
-                             _stream(x))
-        )
+        if h2cache is None:
+            rc = lib.acdc_fwd_f32(_ptr(x), _ptr(y), _ptr(a), _ptr(d), _ptr(bias), x.shape[0], n, _ld(x, n), _ld(y, n),
+                                  _stream(x))
+        else:
+            rc = lib.acdc_fwd_cache_f32(_ptr(x), _ptr(y), _ptr(a), _ptr(d), _ptr(bias), _ptr(h2cache), x.shape[0], n,
+                                        _ld(x, n), _ld(y, n), _stream(x))
+        _lib.check(rc)
     return y
 
 
@@ -95,11 +118,13 @@ def acdc_backward(
     grad_bias: torch.Tensor,
     accumulate: bool = True,
     out=None,
+    h2cache: torch.Tensor | None = None,
 ) -> torch.Tensor:
     """dx and (accumulated) parameter gradients of acdc_forward (layers.py:148-156).
 
     grad_a / grad_d / grad_bias are CUDA fp32 (n,) tensors updated in place:
     ``+=`` when ``accumulate`` (the reference contract), ``=`` otherwise.
+    ``h2cache`` (filled by the matching forward) skips recomputing C2(a * x).
     """
     n = a.shape[0]
     x = _rows2d(x, n)
@@ -118,12 +143,14 @@ def acdc_backward(
         if wsb == 0:
             _lib.check(_lib.ACDC_E_CUDA)
         ws = torch.empty((wsb + 3) // 4, dtype=torch.float32, device=dev)
-        _lib.check(
-            lib.acdc_bwd_f32(
-                _ptr(x), _ptr(dy), _ptr(dx), _ptr(a), _ptr(d), _ptr(grad_a), _ptr(grad_d), _ptr(grad_bias),
-                1 if accumulate else 0, _ptr(ws), wsb, x.shape[0], n, _ld(x, n), _ld(dy, n), _ld(dx, n), _stream(x),
-            )
-        )
+        common = (1 if accumulate else 0, _ptr(ws), wsb, x.shape[0], n, _ld(x, n), _ld(dy, n), _ld(dx, n), _stream(x))
+        if h2cache is None:
+            rc = lib.acdc_bwd_f32(_ptr(x), _ptr(dy), _ptr(dx), _ptr(a), _ptr(d), _ptr(grad_a), _ptr(grad_d),
+                                  _ptr(grad_bias), *common)
+        else:
+            rc = lib.acdc_bwd_cached_f32(_ptr(x), _ptr(dy), _ptr(dx), _ptr(a), _ptr(d), _ptr(h2cache), _ptr(grad_a),
+                                         _ptr(grad_d), _ptr(grad_bias), *common)
+        _lib.check(rc)
     return dx
 
 

@@ -216,3 +216,29 @@ def test_autograd_function():
     assert_close_grad(a.grad, gar, n, rows, "autograd ga")
     assert_close_grad(d.grad, gdr, n, rows, "autograd gd")
     assert_close_grad(b.grad, gbr, n, rows, "autograd gb")
+
+
+@pytest.mark.parametrize("n,rows", [(256, 7), (1024, 64), (4096, 33), (8192, 5), (16384, 3)])
+def test_h2cache_matches_recompute(n, rows):
+    """h2-cache forward/backward (layers.py:145 cache semantics) == recompute path."""
+    from paper_1511_05946_b200 import functional as F
+
+    rng = np.random.default_rng(2000 + n)
+    a, d, b = f32(rng, n, mean=1, std=0.4), f32(rng, n, mean=1, std=0.4), f32(rng, n, std=0.3)
+    x, dy = f32(rng, rows, n), f32(rng, rows, n)
+    xt, dyt, at, dt, bt = map(t32, (x, dy, a, d, b))
+    cache = F.new_h2cache(rows, n, DEV)
+    y = F.acdc_forward(xt, at, dt, bt, h2cache=cache)
+    g = [torch.zeros(n, device=DEV) for _ in range(3)]
+    dx = F.acdc_backward(xt, dyt, at, dt, *g, h2cache=cache)
+    torch.cuda.synchronize()
+    X, A, D, B, DY = (v.astype(np.float64) for v in (x, a, d, b, dy))
+    yr, h2 = O.acdc_forward(X, A, D, B)
+    dxr, gar, gdr, gbr = O.acdc_backward(X, h2, DY, A, D)
+    assert_close_rows(y, yr, n, "y")
+    assert_close_rows(dx, dxr, n, "dx")
+    assert_close_grad(g[0], gar, n, rows, "grad_a")
+    assert_close_grad(g[1], gdr, n, rows, "grad_d")
+    assert_close_grad(g[2], gbr, n, rows, "grad_bias")
+    with pytest.raises(ValueError):
+        F.new_h2cache(4, 128, DEV)
