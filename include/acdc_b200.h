@@ -98,6 +98,27 @@ int acdc_bwd_cached_f32(const float* x, const float* dy, float* dx, const float*
 int acdc_dct2_f32(const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream);
 int acdc_dct3_f32(const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream);
 
+/* ---- Fused ACDC cascade (Cascade over AcdcLayer / ReluLayer / PermutationLayer,
+ * layers.py:309-357, 218-265); 256 <= n <= 16384 ----
+ * Block l (l < depth): u = ACDC_l(x_l) with a/d/bias rows l of [depth][n]
+ * arrays; then ReLU if flags[l] & 1; then x_{l+1}[j] = r[perm_l[j]] if
+ * flags[l] & 2 (perm: [depth][n] int32).  y = output of the last block.
+ * cascade_fwd_f32 runs all blocks in one kernel with activations on chip and
+ * writes checkpoints into ckpt (cascade_ckpt_bytes): x_{l+1} ([depth-1][rows][n],
+ * natural layout, at ckpt) followed by the h2 caches of every block.
+ * The backward is one cascade_bwd_block_f32 per block, last to first: a
+ * cached-h2 ACDC backward of block l (x = x_l, h2cache = block l's cache)
+ * whose epilogue applies block l-1's ReLU (prev_relu) and permutation
+ * (prev_perm, scatter) so dx is already the gradient of block l-1's output. */
+size_t cascade_ckpt_bytes(int64_t rows, int32_t n, int32_t depth);
+int cascade_fwd_f32(const float* x, float* y, int32_t depth, int32_t n, const float* a, const float* d,
+                    const float* bias, const int32_t* perm, const uint8_t* flags, float* ckpt, int64_t rows,
+                    int64_t ldx, int64_t ldy, acdc_stream_t stream);
+int cascade_bwd_block_f32(const float* x, const float* dy, float* dx, const float* a, const float* d,
+                          const float* h2cache, const int32_t* prev_perm, int prev_relu, float* grad_a, float* grad_d,
+                          float* grad_bias, int accumulate, void* ws, size_t ws_bytes, int64_t rows, int32_t n,
+                          int64_t ldx, int64_t ldy, int64_t lddx, acdc_stream_t stream);
+
 /* ---- AFDF: complex diagonals around the FFT pair (layers.py:159-215) ----
  * Rows are complex64, interleaved (re, im); ld in complex elements; a, d, grads
  * are n complex values.  2 <= n <= 16384, 8-byte aligned pointers.

@@ -49,6 +49,13 @@ SIGNATURES = {
     ),
     "acdc_dct2_f32": (ctypes.c_int, [_P, _P, _I64, _I32, _I64, _I64, _P]),
     "acdc_dct3_f32": (ctypes.c_int, [_P, _P, _I64, _I32, _I64, _I64, _P]),
+    "cascade_ckpt_bytes": (ctypes.c_size_t, [_I64, _I32, _I32]),
+    "cascade_fwd_f32": (ctypes.c_int, [_P, _P, _I32, _I32, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _P]),
+    "cascade_bwd_block_f32": (
+        ctypes.c_int,
+        [_P, _P, _P, _P, _P, _P, _P, ctypes.c_int, _P, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _I64, _I32, _I64,
+         _I64, _I64, _P],
+    ),
     "afdf_fwd_c64": (ctypes.c_int, [_P, _P, _P, _P, _I64, _I32, _I64, _I64, _P]),
     "afdf_bwd_workspace_bytes": (ctypes.c_size_t, [_I64, _I32]),
     "afdf_bwd_c64": (

@@ -36,6 +36,8 @@ struct KParams {
   float* ws;          // bwd partials [groups][3][N]
   float* scratch;     // bwd stash when it does not fit in smem [groups][STASH*T]
   float* h2c;         // h2 cache [row pairs][2N] in thread-native layout (H2C kernels)
+  const int* epi_perm;  // bwd epilogue (fused cascade): scatter dx through this permutation
+  int epi_relu;         // bwd epilogue: zero dx where x <= 0 (the previous block's ReLU)
   const float2* tab;  // [pass twiddles | c'_k]
   int64_t rows;
   int64_t ldx, ldy, ldo;
@@ -224,14 +226,15 @@ __global__ void ACDC_LB(Geo<LOGN>) acdc_fwd_kernel(KParams p) {
 // thread-private shared-memory stash (layout [slot][t], conflict-free).  The
 // partials are written once per group to ws and reduced by
 // acdc_grad_reduce_kernel.
-template <int LOGN>
-using GeoBwd = Geo<LOGN, 3 * Geo<LOGN>::E>;  // stash: g3 (E float2) + grad_a (E floats)
+// stash per thread: g3 (E float2, recompute path only) + grad_a partials (E floats)
+template <int LOGN, bool H2C = false>
+using GeoBwd = Geo<LOGN, (H2C ? 1 : 3) * Geo<LOGN>::E>;
 
 // H2C: read h2 from the forward's cache instead of recomputing C2(a * x);
 // the backward then runs 2 packed FFTs instead of 3 and needs no g3 stash.
 template <int LOGN, bool H2C>
-__global__ void ACDC_LB(GeoBwd<LOGN>) acdc_bwd_kernel(KParams p) {
-  using G = GeoBwd<LOGN>;
+__global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
+  using G = GeoBwd<LOGN, H2C>;
   constexpr int E = G::E;
   constexpr int T = G::T;
   constexpr int PL = G::NPASS - 1;
@@ -244,7 +247,7 @@ __global__ void ACDC_LB(GeoBwd<LOGN>) acdc_bwd_kernel(KParams p) {
   Xbuf<G> xb{gbase, 0};
   float* sbase = G::STASH_SMEM ? gbase + G::NBUF * G::BUF_FLOATS : p.scratch + c.gid * G::GSCRATCH_FLOATS;
   float2* st_g3 = reinterpret_cast<float2*>(sbase) + t;  // [E][T]
-  float* st_ga = sbase + 2 * E * T + t;                  // [E][T]
+  float* st_ga = sbase + (H2C ? 0 : 2 * E * T) + t;     // [E][T]
   const float2 *tw, *cp;
   stage_tables<G>(p.tab, smem_f, tw, cp);
   float acc_d[E], acc_b[E];
@@ -348,16 +351,30 @@ __global__ void ACDC_LB(GeoBwd<LOGN>) acdc_bwd_kernel(KParams p) {
       for (int q = 0; q < 8; ++q) {
         const float2 av = ld_f2(pa + 2 * q * S);
         const float2 xav = ld_f2(pxa + 2 * q * S);
-        float s0 = ga[q].x * xav.x, s1 = ga[q].y * xav.y;
-        oa[q * S] = make_float2(av.x * ga[q].x, av.y * ga[q].y);
-        if (hasb) {
-          const float2 xbv = ld_f2(pxb + 2 * q * S);
-          s0 = fmaf(gb[q].x, xbv.x, s0);
-          s1 = fmaf(gb[q].y, xbv.y, s1);
-          ob[q * S] = make_float2(av.x * gb[q].x, av.y * gb[q].y);
+        const float2 xbv = hasb ? ld_f2(pxb + 2 * q * S) : make_float2(0.f, 0.f);
+        st_ga[(2 * q) * T] += fmaf(gb[q].x, xbv.x, ga[q].x * xav.x);
+        st_ga[(2 * q + 1) * T] += fmaf(gb[q].y, xbv.y, ga[q].y * xav.y);
+        float2 da = make_float2(av.x * ga[q].x, av.y * ga[q].y);
+        float2 db = make_float2(av.x * gb[q].x, av.y * gb[q].y);
+        if (p.epi_relu) {  // previous block's ReLU: mask = x > 0 (layers.py:227, 233)
+          da = make_float2(xav.x > 0.f ? da.x : 0.f, xav.y > 0.f ? da.y : 0.f);
+          db = make_float2(xbv.x > 0.f ? db.x : 0.f, xbv.y > 0.f ? db.y : 0.f);
         }
-        st_ga[(2 * q) * T] += s0;
-        st_ga[(2 * q + 1) * T] += s1;
+        if (p.epi_perm) {  // previous block's permutation: out[perm[j]] = g[j] (layers.py:263-265)
+          const int* pp = p.epi_perm + 2 * (fm.jsp + q * S);
+          const int j0 = ld_plain_i(pp), j1 = ld_plain_i(pp + 1);
+          float* ra_ = p.y + ra * p.ldo;
+          float* rb_ = p.y + rb * p.ldo;
+          ra_[j0] = da.x;
+          ra_[j1] = da.y;
+          if (hasb) {
+            rb_[j0] = db.x;
+            rb_[j1] = db.y;
+          }
+        } else {
+          oa[q * S] = da;
+          if (hasb) ob[q * S] = db;
+        }
       }
     }
     // per-group partials
@@ -622,8 +639,9 @@ static LaunchInfo info_for(int kind) {
   const bool bwd = kind == K_BWD || kind == K_BWD_H2;
   li.cta = G::CTA;
   li.gpc = G::GPC;
-  li.scratch = bwd ? GB::GSCRATCH_FLOATS : 0;
-  li.smem = bwd ? GB::SMEM_BYTES : G::SMEM_BYTES;
+  using GBC = GeoBwd<LOGN, FP>;
+  li.scratch = kind == K_BWD ? GB::GSCRATCH_FLOATS : (kind == K_BWD_H2 ? GBC::GSCRATCH_FLOATS : 0);
+  li.smem = kind == K_BWD ? GB::SMEM_BYTES : (kind == K_BWD_H2 ? GBC::SMEM_BYTES : G::SMEM_BYTES);
   return li;
 }
 
@@ -770,7 +788,7 @@ size_t acdc_bwd_workspace_bytes(int64_t rows, int32_t n) {
 static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const float* a, const float* d,
                     const float* h2c, float* grad_a, float* grad_d, float* grad_bias, int accumulate, void* ws,
                     size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, int64_t lddx,
-                    acdc_stream_t stream) {
+                    acdc_stream_t stream, const int32_t* epi_perm = nullptr, int epi_relu = 0) {
   if (kind == K_BWD_H2 && rows > 0 && !h2c) return ACDC_E_NULL;
   int rc = check_common(x, dx, rows, n, ldx, lddx);
   if (rc) return rc;
@@ -792,6 +810,8 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
   p.d = d;
   p.ws = (float*)ws;
   p.h2c = const_cast<float*>(h2c);
+  p.epi_perm = epi_perm;
+  p.epi_relu = epi_relu;
   p.rows = rows;
   p.ldx = ldx;
   p.ldy = ldy;
@@ -838,6 +858,16 @@ int acdc_bwd_cached_f32(const float* x, const float* dy, float* dx, const float*
   if (acdc_h2cache_bytes(rows, n) == 0) return set_error(ACDC_E_SIZE, "the h2 cache needs n >= 256 and n <= 16384");
   return bwd_impl(K_BWD_H2, x, dy, dx, a, d, h2cache, grad_a, grad_d, grad_bias, accumulate, ws, ws_bytes, rows, n,
                   ldx, ldy, lddx, stream);
+}
+
+int cascade_bwd_block_f32(const float* x, const float* dy, float* dx, const float* a, const float* d,
+                          const float* h2cache, const int32_t* prev_perm, int prev_relu, float* grad_a, float* grad_d,
+                          float* grad_bias, int accumulate, void* ws, size_t ws_bytes, int64_t rows, int32_t n,
+                          int64_t ldx, int64_t ldy, int64_t lddx, acdc_stream_t stream) {
+  if (acdc_h2cache_bytes(rows, n) == 0) return set_error(ACDC_E_SIZE, "the fused cascade needs 256 <= n <= 16384");
+  if (prev_perm && dx == dy) return set_error(ACDC_E_SHAPE, "the permuted epilogue cannot write in place");
+  return bwd_impl(K_BWD_H2, x, dy, dx, a, d, h2cache, grad_a, grad_d, grad_bias, accumulate, ws, ws_bytes, rows, n,
+                  ldx, ldy, lddx, stream, prev_perm, prev_relu);
 }
 
 static int transform(int kind, const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy,

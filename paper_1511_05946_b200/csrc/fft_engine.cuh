@@ -25,9 +25,9 @@
 #include <cuda_runtime.h>
 
 #ifdef ACDC_NO_LB  // experiments: report the natural register demand
-#define ACDC_LB(G)
+#define ACDC_LB(...)
 #else
-#define ACDC_LB(G) __launch_bounds__(G::CTA, G::MINB)
+#define ACDC_LB(...) __launch_bounds__(__VA_ARGS__::CTA, __VA_ARGS__::MINB)
 #endif
 
 namespace acdc {

@@ -30,6 +30,9 @@ __all__ = [
     "prepare",
     "h2cache_supported",
     "new_h2cache",
+    "cascade_supported",
+    "cascade_forward",
+    "cascade_backward",
 ]
 
 
@@ -290,3 +293,75 @@ class AfdfFunction(torch.autograd.Function):
 def afdf(x, a, d):
     """Differentiable AFDF layer: ``AfdfFunction.apply``."""
     return AfdfFunction.apply(x, a, d)
+
+
+# ----------------------------------------------------------- fused cascade
+
+
+def cascade_supported(n: int) -> bool:
+    return h2cache_supported(n)
+
+
+def cascade_forward(x: torch.Tensor, a: torch.Tensor, d: torch.Tensor, bias: torch.Tensor, perm: torch.Tensor | None,
+                    flags: torch.Tensor, out=None):
+    """Fused forward of ``depth`` blocks  x <- perm(relu(ACDC(x)))  (layers.py:336-339).
+
+    a, d, bias: (depth, n) fp32; perm: (depth, n) int32 or None; flags: (depth,)
+    uint8 (bit0 ReLU, bit1 permutation after the block).  Returns (y, ckpt)
+    where ckpt holds the per-block checkpoints for :func:`cascade_backward`."""
+    depth, n = a.shape
+    x = _rows2d(x, n)
+    dev = x.device
+    a, d, bias = (v.to(device=dev, dtype=torch.float32).contiguous() for v in (a, d, bias))
+    lib = _lib.load()
+    nbytes = lib.cascade_ckpt_bytes(x.shape[0], n, depth)
+    if nbytes == 0:
+        raise ValueError(f"the fused cascade needs 256 <= n <= 16384, got {n}")
+    ckpt = torch.empty(nbytes // 4, dtype=torch.float32, device=dev)
+    y = torch.empty_like(x, memory_format=torch.contiguous_format) if out is None else out
+    with torch.cuda.device(dev):
+        _lib.check(lib.cascade_fwd_f32(_ptr(x), _ptr(y), depth, n, _ptr(a), _ptr(d), _ptr(bias), _ptr(perm),
+                                       _ptr(flags), _ptr(ckpt), x.shape[0], _ld(x, n), _ld(y, n), _stream(x)))
+    return y, ckpt
+
+
+def _ckpt_views(ckpt: torch.Tensor, rows: int, n: int, depth: int):
+    xs = ckpt[: (depth - 1) * rows * n].view(depth - 1, rows, n) if depth > 1 else None
+    per = ((rows + 1) // 2) * 2 * n
+    base = (depth - 1) * rows * n
+    h2 = [ckpt[base + l * per: base + (l + 1) * per] for l in range(depth)]
+    return xs, h2
+
+
+def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor | None, flags,
+                     ckpt: torch.Tensor, grads, accumulate: bool = True) -> torch.Tensor:
+    """Backward of :func:`cascade_forward` (layers.py:341-344): one cached-h2
+    block backward per block, last to first, each applying the previous block's
+    ReLU mask and inverse permutation in its epilogue.  ``a``, ``d``: sequences
+    of (n,) tensors per block; ``grads``: per block (grad_a, grad_d, grad_bias)
+    fp32 (n,) tensors, accumulated in place; ``flags``: host list of ints."""
+    depth = len(a)
+    n = a[0].shape[0]
+    x = _rows2d(x, n)
+    g = _rows2d(dy, n, "grad_y")
+    rows = x.shape[0]
+    dev = x.device
+    xs, h2 = _ckpt_views(ckpt, rows, n, depth)
+    fl = [int(f) for f in flags]
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        wsb = lib.acdc_bwd_workspace_bytes(rows, n)
+        ws = torch.empty((wsb + 3) // 4, dtype=torch.float32, device=dev)
+        for l in range(depth - 1, -1, -1):
+            xl = x if l == 0 else xs[l - 1]
+            prev = fl[l - 1] if l > 0 else 0
+            pp = perm[l - 1] if (l > 0 and prev & 2) else None
+            out = torch.empty_like(g)
+            ga, gd, gb = grads[l]
+            al, dl = _vec(a[l], n, dev, "a"), _vec(d[l], n, dev, "d")
+            _lib.check(lib.cascade_bwd_block_f32(
+                _ptr(xl), _ptr(g), _ptr(out), _ptr(al), _ptr(dl), _ptr(h2[l]), _ptr(pp), 1 if prev & 1 else 0,
+                _ptr(ga), _ptr(gd), _ptr(gb), 1 if accumulate else 0, _ptr(ws), wsb, rows, n, _ld(xl, n), _ld(g, n),
+                n, _stream(x)))
+            g = out
+    return g

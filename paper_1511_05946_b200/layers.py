@@ -118,7 +118,8 @@ class Layer:
     def _out(y: torch.Tensor, host: bool):
         if not host:
             return y
-        return y.detach().to("cpu", dtype=torch.float64).numpy()
+        dt = torch.complex128 if y.is_complex() else torch.float64
+        return y.detach().to("cpu", dtype=dt).numpy()
 
 
 class AcdcLayer(Layer):
@@ -349,6 +350,46 @@ class Cascade:
             raise ValueError("cannot mix complex and real layers in one cascade")
         self.layers = layers
         self.complex_domain = any(l.complex_domain for l in layers)
+        self._fused = self._fusion_plan(layers)
+        self._cache = None
+
+    @staticmethod
+    def _fusion_plan(layers):
+        """Blocks (ACDC [, ReLU] [, Perm]) covering the whole stack, ending in an
+        ACDC layer, at a size the fused cascade kernels support; else None."""
+        if not layers or not isinstance(layers[-1], AcdcLayer):
+            return None
+        n = layers[0].n_in
+        if not F.cascade_supported(n) or any(l.n_in != n for l in layers):
+            return None
+        blocks, i = [], 0
+        while i < len(layers):
+            if not isinstance(layers[i], AcdcLayer):
+                return None
+            blk = [layers[i], None, None]
+            i += 1
+            if i < len(layers) and isinstance(layers[i], ReluLayer):
+                blk[1] = layers[i]
+                i += 1
+            if i < len(layers) and isinstance(layers[i], PermutationLayer):
+                blk[2] = layers[i]
+                i += 1
+            blocks.append(blk)
+        dev = blocks[0][0].device
+        if any(b[0].device != dev for b in blocks):
+            return None
+        flags = [(1 if b[1] is not None else 0) | (2 if b[2] is not None else 0) for b in blocks]
+        perm = None
+        if any(f & 2 for f in flags):
+            rows = [torch.as_tensor(b[2].perm if b[2] is not None else np.arange(n), dtype=torch.int32) for b in blocks]
+            perm = torch.stack(rows).to(dev).contiguous()
+        return {"blocks": blocks, "flags": flags, "flags_t": torch.tensor(flags, dtype=torch.uint8, device=dev),
+                "perm": perm, "n": n, "device": dev}
+
+    @property
+    def fused(self) -> bool:
+        """True when forward/backward run the fused cascade kernels."""
+        return self._fused is not None
 
     @property
     def n_in(self):
@@ -360,17 +401,39 @@ class Cascade:
 
     def forward(self, x):
         host = not (isinstance(x, torch.Tensor) and x.is_cuda)
+        if self._fused is not None:
+            fz = self._fused
+            xt, _ = self.layers[0]._check_input(x)
+            acdc = [b[0] for b in fz["blocks"]]
+            a = torch.stack([l.a for l in acdc])
+            d = torch.stack([l.d for l in acdc])
+            bias = torch.stack([l.bias_d for l in acdc])
+            y, ckpt = F.cascade_forward(xt, a, d, bias, fz["perm"], fz["flags_t"])
+            self._cache = (xt, ckpt)
+            return Layer._out(y, host)
+        if host:
+            x, _ = self.layers[0]._check_input(x, torch.complex64 if self.complex_domain else torch.float32)
         for layer in self.layers:
-            x = layer.forward(x if not isinstance(x, np.ndarray) else x)
-            if isinstance(x, np.ndarray):  # keep intermediates on device
-                x = torch.as_tensor(x, dtype=torch.float32, device=layer.device)
+            x = layer.forward(x)
         return Layer._out(x, host)
 
     def backward(self, grad_y, retain_cache=False):
         host = not (isinstance(grad_y, torch.Tensor) and grad_y.is_cuda)
+        if self._fused is not None:
+            if self._cache is None:
+                raise RuntimeError("Cascade.backward called before forward")
+            xt, ckpt = self._cache
+            if not retain_cache:
+                self._cache = None
+            gy, _ = self.layers[-1]._check_input(grad_y)
+            fz = self._fused
+            acdc = [b[0] for b in fz["blocks"]]
+            dx = F.cascade_backward(xt, gy, [l.a for l in acdc], [l.d for l in acdc], fz["perm"], fz["flags"], ckpt,
+                                    [(l.grad_a, l.grad_d, l.grad_bias_d) for l in acdc], accumulate=True)
+            return Layer._out(dx, host)
         g = grad_y
         if host:
-            g = torch.as_tensor(np.asarray(grad_y), dtype=torch.float32).to(self.layers[-1].device)
+            g, _ = self.layers[-1]._check_input(grad_y, torch.complex64 if self.complex_domain else torch.float32)
         for layer in reversed(self.layers):
             g = layer.backward(g, retain_cache=retain_cache)
         return Layer._out(g, host)
