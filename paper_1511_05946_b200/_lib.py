@@ -13,7 +13,8 @@ import os
 import threading
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libacdc_b200.so")
+# ACDC_LIB_PATH selects an alternative build of the same ABI (A/B kernel experiments)
+LIB_PATH = os.environ.get("ACDC_LIB_PATH") or os.path.join(_PKG, "libacdc_b200.so")
 
 ACDC_OK = 0
 ACDC_E_SIZE = -1

@@ -120,11 +120,27 @@ __device__ __forceinline__ void packed_dct3(float2 (&Y)[G::E], float2 (&v)[G::E]
 
 // y = C3(d * C2(a * x) + bias)          (layers.py:141-146)
 // H2C: also store h2 = C2(a * x) (the reference's cache, layers.py:145) in a
-// thread-native layout: row pair rp, slot i, thread t at h2c[rp*2N + 2*(i*T + t)]
-// as (rowA, rowB).  Only the fast-pairing sizes (N >= 256) support it.
+// thread-native layout: row pair rp, frequency slot s, thread t at
+// h2c[rp*2N + 4*(s*T + t)] as (lo.A, lo.B, hi.A, hi.B).  Only the fast-pairing sizes (N >= 256) support it.
+// Threads per CTA on the fast-pairing path: the forward runs 768-thread CTAs
+// (24 warps/SM, 85-register cap, single-buffered exchanges), ~10% faster than
+// 512 at N=4096 in an interleaved A/B (scripts/ab_bench.py).  0 = default.
+#ifndef ACDC_FWD_CTA
+#define ACDC_FWD_CTA 768
+#endif
+#ifndef ACDC_BWD_CTA
+#define ACDC_BWD_CTA 0
+#endif
+template <int LOGN, int CTA>
+constexpr int fp_gpc() {
+  return (CTA && Geo<LOGN>::FP && Geo<LOGN>::T <= CTA / 2) ? CTA / Geo<LOGN>::T : 0;
+}
+template <int LOGN>
+using GeoFwd = Geo<LOGN, 0, fp_gpc<LOGN, ACDC_FWD_CTA>()>;
+
 template <int LOGN, bool H2C>
-__global__ void ACDC_LB(Geo<LOGN>) acdc_fwd_kernel(KParams p) {
-  using G = Geo<LOGN>;
+__global__ void ACDC_LB(GeoFwd<LOGN>) acdc_fwd_kernel(KParams p) {
+  using G = GeoFwd<LOGN>;
   constexpr int E = G::E;
   constexpr int PL = G::NPASS - 1;
   extern __shared__ __align__(16) float smem_f[];
@@ -158,9 +174,8 @@ __global__ void ACDC_LB(Geo<LOGN>) acdc_fwd_kernel(KParams p) {
           float2 xl, xh;
           dct2_post(v[s], w[s], cs, fm.special(s), chi, xl, xh);
           if constexpr (H2C) {
-            float2* hc = reinterpret_cast<float2*>(p.h2c + rp * 2 * G::N) + t;
-            hc[(2 * s) * G::T] = xl;
-            hc[(2 * s + 1) * G::T] = xh;
+            float4* hc = reinterpret_cast<float4*>(p.h2c + rp * 2 * G::N) + t;  // [slot s][t]
+            __stcs(hc + s * G::T, make_float4(xl.x, xl.y, xh.x, xh.y));
           }
           const float dl = ld_plain(fm.plo(p.d, s)), bl = ld_plain(fm.plo(p.bias, s));
           const float dh = ld_plain(fm.phi(p.d, s)), bh = ld_plain(fm.phi(p.bias, s));
@@ -228,7 +243,7 @@ __global__ void ACDC_LB(Geo<LOGN>) acdc_fwd_kernel(KParams p) {
 // acdc_grad_reduce_kernel.
 // stash per thread: g3 (E float2, recompute path only) + grad_a partials (E floats)
 template <int LOGN, bool H2C = false>
-using GeoBwd = Geo<LOGN, (H2C ? 1 : 3) * Geo<LOGN>::E>;
+using GeoBwd = Geo<LOGN, (H2C ? 1 : 3) * Geo<LOGN>::E, (H2C ? fp_gpc<LOGN, ACDC_BWD_CTA>() : 0)>;
 
 // H2C: read h2 from the forward's cache instead of recomputing C2(a * x);
 // the backward then runs 2 packed FFTs instead of 3 and needs no g3 stash.
@@ -286,7 +301,7 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
         // g3 and the cached h2 in one slot pass: grad_bias, grad_d, Y = d * g3
         float2 w[8], gl[8], gh[8];
         fp_partner<G>(v, w, fm);
-        const float2* hc = reinterpret_cast<const float2*>(p.h2c + rp * 2 * G::N) + t;
+        const float4* hc = reinterpret_cast<const float4*>(p.h2c + rp * 2 * G::N) + t;
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
           const float2 cs = tab_load<G>(fm.plo(cp, s), 0);
@@ -294,7 +309,8 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
           dct2_post(v[s], w[s], cs, fm.special(s), chi, g3l, g3h);
           acc_b[2 * s] += g3l.x + g3l.y;
           acc_b[2 * s + 1] += g3h.x + g3h.y;
-          const float2 hl = __ldcs(hc + (2 * s) * G::T), hh = __ldcs(hc + (2 * s + 1) * G::T);
+          const float4 h4 = __ldcs(hc + s * G::T);
+          const float2 hl = make_float2(h4.x, h4.y), hh = make_float2(h4.z, h4.w);
           acc_d[2 * s] = fmaf(hl.x, g3l.x, fmaf(hl.y, g3l.y, acc_d[2 * s]));
           acc_d[2 * s + 1] = fmaf(hh.x, g3h.x, fmaf(hh.y, g3h.y, acc_d[2 * s + 1]));
           const float dl = ld_plain(fm.plo(p.d, s)), dh = ld_plain(fm.phi(p.d, s));
@@ -624,24 +640,48 @@ __global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __re
 
 enum Kind { K_FWD = 0, K_BWD = 1, K_DCT2 = 2, K_DCT3 = 3, K_FWD_H2 = 4, K_BWD_H2 = 5 };
 
+template <class K>
+static void geom(LaunchInfo& li, int scratch) {
+  li.cta = K::CTA;
+  li.gpc = K::GPC;
+  li.smem = K::SMEM_BYTES;
+  li.scratch = scratch;
+}
+
 template <int LOGN>
 static LaunchInfo info_for(int kind) {
   using G = Geo<LOGN>;
-  using GB = GeoBwd<LOGN>;
-  LaunchInfo li;
   constexpr bool FP = G::FP;  // the h2 cache exists only on the fast-pairing path
-  li.fn = kind == K_FWD      ? (const void*)acdc_fwd_kernel<LOGN, false>
-          : kind == K_BWD    ? (const void*)acdc_bwd_kernel<LOGN, false>
-          : kind == K_DCT2   ? (const void*)acdc_dct2_kernel<LOGN>
-          : kind == K_DCT3   ? (const void*)acdc_dct3_kernel<LOGN>
-          : kind == K_FWD_H2 ? (FP ? (const void*)acdc_fwd_kernel<LOGN, FP> : nullptr)
-                             : (FP ? (const void*)acdc_bwd_kernel<LOGN, FP> : nullptr);
-  const bool bwd = kind == K_BWD || kind == K_BWD_H2;
-  li.cta = G::CTA;
-  li.gpc = G::GPC;
+  using GF = GeoFwd<LOGN>;
+  using GB = GeoBwd<LOGN, false>;
   using GBC = GeoBwd<LOGN, FP>;
-  li.scratch = kind == K_BWD ? GB::GSCRATCH_FLOATS : (kind == K_BWD_H2 ? GBC::GSCRATCH_FLOATS : 0);
-  li.smem = kind == K_BWD ? GB::SMEM_BYTES : (kind == K_BWD_H2 ? GBC::SMEM_BYTES : G::SMEM_BYTES);
+  LaunchInfo li;
+  switch (kind) {
+    case K_FWD:
+      li.fn = (const void*)acdc_fwd_kernel<LOGN, false>;
+      geom<GF>(li, 0);
+      break;
+    case K_BWD:
+      li.fn = (const void*)acdc_bwd_kernel<LOGN, false>;
+      geom<GB>(li, GB::GSCRATCH_FLOATS);
+      break;
+    case K_DCT2:
+      li.fn = (const void*)acdc_dct2_kernel<LOGN>;
+      geom<G>(li, 0);
+      break;
+    case K_DCT3:
+      li.fn = (const void*)acdc_dct3_kernel<LOGN>;
+      geom<G>(li, 0);
+      break;
+    case K_FWD_H2:
+      li.fn = FP ? (const void*)acdc_fwd_kernel<LOGN, FP> : nullptr;
+      geom<GF>(li, 0);
+      break;
+    default:
+      li.fn = FP ? (const void*)acdc_bwd_kernel<LOGN, FP> : nullptr;
+      geom<GBC>(li, GBC::GSCRATCH_FLOATS);
+      break;
+  }
   return li;
 }
 

@@ -89,14 +89,13 @@ __global__ void ACDC_LB(Geo<LOGN>) cascade_fwd_kernel(CParams p) {
       {
         float2 w[8], gl[8], gh[8];
         fp_partner<G>(v, w, fm);
-        float2* hc = reinterpret_cast<float2*>(p.h2c + ((int64_t)l * npairs + rp) * 2 * N) + t;
+        float4* hc = reinterpret_cast<float4*>(p.h2c + ((int64_t)l * npairs + rp) * 2 * N) + t;
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
           const float2 cs = tab_load<G>(fm.plo(cp, s), 0);
           float2 xl, xh;
           dct2_post(v[s], w[s], cs, fm.special(s), chi, xl, xh);
-          hc[(2 * s) * T] = xl;
-          hc[(2 * s + 1) * T] = xh;
+          __stcs(hc + s * T, make_float4(xl.x, xl.y, xh.x, xh.y));
           const float dlo = ld_plain(fm.plo(dl, s)), blo = ld_plain(fm.plo(bl, s));
           const float dhi = ld_plain(fm.phi(dl, s)), bhi = ld_plain(fm.phi(bl, s));
           xl = make_float2(fmaf(xl.x, dlo, blo), fmaf(xl.y, dlo, blo));

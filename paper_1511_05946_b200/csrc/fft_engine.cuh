@@ -147,9 +147,12 @@ struct Plan {
   __host__ __device__ static constexpr int span(int p) {  // Ns before pass p
     return p == 0 ? 1 : span(p - 1) * radix(p - 1);
   }
-  // pass p >= 1 twiddles W_{Ns R}^{q k}, stored at tw_off(p) + (q-1)*Ns + k
+  // pass p >= 1 twiddles W_{Ns R}^{q k}, stored at tw_off(p) + k*tw_stride(R) + (q-1):
+  // one row per butterfly k so consecutive q pairs load as one 128-bit LDS; the
+  // row stride (R+2 float2, or 1 for R = 2) keeps 8 consecutive k on disjoint banks.
+  __host__ __device__ static constexpr int tw_stride(int r) { return r == 2 ? 1 : r + 2; }
   __host__ __device__ static constexpr int tw_off(int p) {
-    return p <= 1 ? 0 : tw_off(p - 1) + (radix(p - 1) - 1) * span(p - 1);
+    return p <= 1 ? 0 : tw_off(p - 1) + tw_stride(radix(p - 1)) * span(p - 1);
   }
   static constexpr int TW_ENTRIES = tw_off(NPASS);  // float2 entries (0 for one pass)
   static constexpr int CP_ENTRIES = N / 2 + 1;      // DCT post-twiddles c'_k
@@ -162,13 +165,13 @@ struct Plan {
 // hold GPC row-pair groups (512 threads when T <= 512) sharing one copy of the
 // tables; the plan prefers tables in smem and double-buffered exchanges and
 // falls back (single buffer, tables in global) until the CTA fits in 227 KB.
-template <int LOGN, int STASH = 0>
+template <int LOGN, int STASH = 0, int GPCX = 0>
 struct Geo : Plan<LOGN> {
   using P_ = Plan<LOGN>;
   static constexpr int N = 1 << LOGN;
   static constexpr int E = LOGN >= 15 ? 32 : (N >= 16 ? 16 : N);  // complex values per thread
   static constexpr int T = N / E;                                 // threads per row-pair group
-  static constexpr int GPC = T <= 512 ? 512 / T : 1;              // groups per CTA
+  static constexpr int GPC = GPCX ? GPCX : (T <= 512 ? 512 / T : 1);  // groups per CTA
   static constexpr int CTA = T * GPC;                             // threads per CTA
   static constexpr int PADN = N + N / 16;                         // padded float2 slots per buffer
   static constexpr bool SPLIT = (N >= 32768);                     // exchange re / im separately
@@ -242,6 +245,17 @@ __device__ __forceinline__ float2 tab_load(const float2* tab, int i) {
     return tab[i];
   } else {
     return ldg_f2_volatile(tab + i);
+  }
+}
+
+template <class G>
+__device__ __forceinline__ float4 tab_load4(const float2* tab) {
+  if constexpr (G::TW_SMEM) {
+    return *reinterpret_cast<const float4*>(tab);
+  } else {
+    float4 r;
+    asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(tab));
+    return r;
   }
 }
 
@@ -319,9 +333,17 @@ __device__ __forceinline__ void pass_compute(float2 (&v)[G::E], const float2* tw
   for (int b = 0; b < NB; ++b) {
     if constexpr (NS > 1) {
       const int k = (j0 + b * G::T) & (NS - 1);
-      const float2* row = tw + G::tw_off(P) + k;  // row[(q-1)*NS] = W_{NS R}^{q k}
+      const float2* row = tw + G::tw_off(P) + k * G::tw_stride(R);  // row[q-1] = W_{NS R}^{q k}
+      if constexpr (R == 2) {
+        v[b * R + 1] = cmul(v[b * R + 1], tab_load<G>(row, 0));
+      } else {
 #pragma unroll
-      for (int q = 1; q < R; ++q) v[b * R + q] = cmul(v[b * R + q], tab_load<G>(row, (q - 1) * NS));
+        for (int q = 1; q < R; q += 2) {
+          const float4 w2 = tab_load4<G>(row + (q - 1));
+          v[b * R + q] = cmul(v[b * R + q], make_float2(w2.x, w2.y));
+          if (q + 1 < R) v[b * R + q + 1] = cmul(v[b * R + q + 1], make_float2(w2.z, w2.w));
+        }
+      }
     }
     dft<R>(&v[b * R]);
   }

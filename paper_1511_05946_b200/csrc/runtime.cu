@@ -81,12 +81,15 @@ int get_tables(int logn, Tables* out) {
   const int n = 1 << logn;
   std::vector<int> radix;
   host_plan(logn, radix);
+  // per-pass [k][q] twiddle rows, stride Plan::tw_stride(R) (fft_engine.cuh)
   std::vector<float2> h;
   long ns = radix[0];
   for (size_t p = 1; p < radix.size(); ++p) {
     const int r = radix[p];
-    for (int q = 1; q < r; ++q)
-      for (long k = 0; k < ns; ++k) h.push_back(twiddle((long)q * k, ns * r));
+    const int stride = r == 2 ? 1 : r + 2;
+    for (long k = 0; k < ns; ++k)
+      for (int slot = 0; slot < stride; ++slot)
+        h.push_back(slot < r - 1 ? twiddle((long)(slot + 1) * k, ns * r) : make_float2(0.f, 0.f));
     ns *= r;
   }
   const double pi = 3.14159265358979323846264338327950288;
