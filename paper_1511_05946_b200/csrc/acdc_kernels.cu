@@ -819,10 +819,18 @@ size_t acdc_bwd_workspace_bytes(int64_t rows, int32_t n) {
   int logn;
   if (check_n(n, &logn)) return 0;
   if (logn == 0) return 3 * sizeof(float);
-  LaunchInfo li;
-  int64_t grid;
-  if (sized(logn, K_BWD, rows > 0 ? rows : 1, &li, &grid)) return 0;
-  return (size_t)grid * li.gpc * (3 * (size_t)n + (size_t)li.scratch) * sizeof(float);
+  // large enough for both backward kernels (recompute and h2-cache differ in
+  // groups per CTA and stash placement)
+  size_t best = 0;
+  for (int kind : {K_BWD, K_BWD_H2}) {
+    LaunchInfo li;
+    int64_t grid;
+    if (launch_info(logn, kind, &li) || !li.fn) continue;
+    if (grid_for(li, ((rows > 0 ? rows : 1) + 1) / 2, &grid)) return 0;
+    const size_t b = (size_t)grid * li.gpc * (3 * (size_t)n + (size_t)li.scratch) * sizeof(float);
+    best = b > best ? b : best;
+  }
+  return best;
 }
 
 static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const float* a, const float* d,
