@@ -33,6 +33,7 @@ __all__ = [
     "cascade_supported",
     "cascade_forward",
     "cascade_backward",
+    "HostPipeline",
 ]
 
 
@@ -365,3 +366,75 @@ def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor
                 n, _stream(x)))
             g = out
     return g
+
+
+# ------------------------------------------------- host-buffer pipelined step
+
+
+class HostPipeline:
+    """Forward + backward of one ACDC layer on HOST (pinned) buffers, with the
+    batch split into chunks so host->device copies, kernels and device->host
+    copies of different chunks overlap on three streams (PCIe is full duplex).
+
+    ``step(x_host, dy_host, y_host, dx_host)`` computes y = layer(x) and dx,
+    writes them back to host, and accumulates the parameter gradients into
+    ``grads`` (device, summed over all chunks: the reference's "+=" semantics).
+    Chunks are independent rows, so the result equals one full-batch call.
+    """
+
+    def __init__(self, n: int, rows: int, device, chunks: int = 8, h2cache: bool = True):
+        self.n, self.rows, self.dev = n, rows, torch.device(device)
+        self.chunks = max(1, min(chunks, rows))
+        bounds = torch.linspace(0, rows, self.chunks + 1).long().tolist()
+        self.spans = [(bounds[i], bounds[i + 1]) for i in range(self.chunks) if bounds[i + 1] > bounds[i]]
+        mx = max(b - a for a, b in self.spans)
+        # two device buffer sets so chunk i+1 uploads while chunk i computes
+        self.xd = [torch.empty(mx, n, device=self.dev) for _ in range(2)]
+        self.dyd = [torch.empty(mx, n, device=self.dev) for _ in range(2)]
+        self.yd = [torch.empty(mx, n, device=self.dev) for _ in range(2)]
+        self.dxd = [torch.empty(mx, n, device=self.dev) for _ in range(2)]
+        self.hc = [new_h2cache(mx, n, self.dev) for _ in range(2)] if (h2cache and h2cache_supported(n)) else None
+        self.s_in = torch.cuda.Stream(self.dev)
+        self.s_cmp = torch.cuda.Stream(self.dev)
+        self.s_out = torch.cuda.Stream(self.dev)
+        prepare(n, self.dev)
+
+    def step(self, x_host, dy_host, y_host, dx_host, a, d, bias, grads, accumulate=True):
+        """All host tensors must be pinned CPU fp32 (rows, n).  Returns after
+        enqueueing; call ``torch.cuda.synchronize()`` (or an event) to wait."""
+        ga, gd, gb = grads
+        if not accumulate:
+            with torch.cuda.stream(self.s_cmp):
+                ga.zero_()
+                gd.zero_()
+                gb.zero_()
+        up = [torch.cuda.Event() for _ in self.spans]
+        done = [torch.cuda.Event() for _ in self.spans]
+        down = [torch.cuda.Event() for _ in self.spans]
+        cur = torch.cuda.current_stream(self.dev)
+        for s in (self.s_in, self.s_cmp, self.s_out):
+            s.wait_stream(cur)
+        for i, (lo, hi) in enumerate(self.spans):
+            k, m = i % 2, hi - lo
+            with torch.cuda.stream(self.s_in):
+                if i >= 2:  # buffer set k is free once chunk i-2 was computed
+                    self.s_in.wait_event(done[i - 2])
+                self.xd[k][:m].copy_(x_host[lo:hi], non_blocking=True)
+                self.dyd[k][:m].copy_(dy_host[lo:hi], non_blocking=True)
+                up[i].record(self.s_in)
+            with torch.cuda.stream(self.s_cmp):
+                self.s_cmp.wait_event(up[i])
+                if i >= 2:  # outputs of chunk i-2 must be downloaded first
+                    self.s_cmp.wait_event(down[i - 2])
+                hc = self.hc[k] if self.hc is not None else None
+                acdc_forward(self.xd[k][:m], a, d, bias, out=self.yd[k][:m], h2cache=hc)
+                acdc_backward(self.xd[k][:m], self.dyd[k][:m], a, d, ga, gd, gb, accumulate=True,
+                              out=self.dxd[k][:m], h2cache=hc)
+                done[i].record(self.s_cmp)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(done[i])
+                y_host[lo:hi].copy_(self.yd[k][:m], non_blocking=True)
+                dx_host[lo:hi].copy_(self.dxd[k][:m], non_blocking=True)
+                down[i].record(self.s_out)
+        for s in (self.s_in, self.s_cmp, self.s_out):
+            cur.wait_stream(s)

@@ -242,3 +242,27 @@ def test_h2cache_matches_recompute(n, rows):
     assert_close_grad(g[2], gbr, n, rows, "grad_bias")
     with pytest.raises(ValueError):
         F.new_h2cache(4, 128, DEV)
+
+
+def test_host_pipeline_matches_device_path():
+    """functional.HostPipeline (chunked H2D / kernels / D2H overlap) == one device call."""
+    from paper_1511_05946_b200 import functional as F
+
+    n, rows = 1024, 300
+    rng = np.random.default_rng(21)
+    x, dy = f32(rng, rows, n), f32(rng, rows, n)
+    a, d, b = (t32(f32(rng, n, mean=m, std=0.3)) for m in (1.0, 1.0, 0.0))
+    pipe = F.HostPipeline(n, rows, DEV, chunks=5)
+    xh, dyh = torch.as_tensor(x).pin_memory(), torch.as_tensor(dy).pin_memory()
+    yh, dxh = torch.empty(rows, n).pin_memory(), torch.empty(rows, n).pin_memory()
+    g = [torch.zeros(n, device=DEV) for _ in range(3)]
+    pipe.step(xh, dyh, yh, dxh, a, d, b, g, accumulate=False)
+    torch.cuda.synchronize()
+    g2 = [torch.zeros(n, device=DEV) for _ in range(3)]
+    y2 = F.acdc_forward(t32(x), a, d, b)
+    dx2 = F.acdc_backward(t32(x), t32(dy), a, d, *g2)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(yh, y2.cpu(), rtol=1e-6, atol=1e-6)
+    torch.testing.assert_close(dxh, dx2.cpu(), rtol=1e-6, atol=1e-6)
+    for u, v in zip(g, g2):
+        torch.testing.assert_close(u, v, rtol=1e-5, atol=1e-4)
