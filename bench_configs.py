@@ -181,18 +181,15 @@ def c4(args, dev):
     casc, layers = _cascade(n, depth, False, dev, rng)
     x = torch.randn(B, n, device=dev)
     target = torch.randn(B, n, device=dev)
-    params = casc.params()
-    vel = [torch.zeros_like(p.value) for p in params]
-    lr, mu = 1e-3, 0.9
+    from paper_1511_05946_b200.training import Sgd, SgdConfig
+
+    opt = Sgd(casc.params(), SgdConfig(learning_rate=1e-3, momentum=0.9))  # training.py:58-84
 
     def step():
-        casc.zero_grads()
         y = casc.forward(x)
         gy = (2.0 / y.numel()) * (y - target)  # mse_loss gradient (training.py:176-183)
         casc.backward(gy)
-        for p, v in zip(params, vel):  # Sgd.step, diagonals undecayed
-            v.mul_(mu).add_(p.grad, alpha=-lr)
-            p.value.add_(v)
+        opt.step()  # momentum SGD, zeroes the grads
 
     ms = timeit(step, max(3, args.steps // 10))
     return {"config": "C4 deep SELL 32 ACDC layers N=4096 train step (1 GPU of the DP job)", "fused": casc.fused,

@@ -143,3 +143,34 @@ def test_ref_kernels_agree_with_oracle():
     dxo, gao, gdo, gbo = O.acdc_backward(x, h2, dy, a, d)
     for m, r in ((y, yo), (dx, dxo), (ga, gao), (gd, gdo), (gb, gbo)):
         np.testing.assert_allclose(m, r, atol=1e-12)
+
+
+def test_sgd_matches_reference_update():
+    """paper_1511_05946_b200.training.Sgd == training.py:72-84 (oracle.sgd_step), CPU tensors."""
+    import torch
+
+    from paper_1511_05946_b200.layers import Param
+    from paper_1511_05946_b200.training import Sgd, SgdConfig
+
+    rng = np.random.default_rng(4)
+    vals = [rng.standard_normal(5) for _ in range(3)]
+    grads = [rng.standard_normal(5) for _ in range(3)]
+    decay = [False, True, False]
+    mult = [1.0, 0.5, 2.0]
+    ps = [Param(f"p{i}", torch.tensor(v), torch.tensor(g), decay=dc, lr_mult=m)
+          for i, (v, g, dc, m) in enumerate(zip(vals, grads, decay, mult))]
+    cfg = SgdConfig(learning_rate=0.1, momentum=0.9, weight_decay=0.01, lr_decay_factor=0.5, lr_decay_every=2)
+    opt = Sgd(ps, cfg)
+    ref_v = [np.zeros(5) for _ in range(3)]
+    ref_p = [v.copy() for v in vals]
+    for step in range(3):
+        gs = [rng.standard_normal(5) for _ in range(3)]
+        for p, g in zip(ps, gs):
+            p.grad.copy_(torch.tensor(g))
+        opt.step()
+        for i in range(3):
+            gg = gs[i].copy()
+            O.sgd_step(ref_p[i], gg, ref_v[i], cfg.effective_lr(step), cfg.momentum, cfg.weight_decay, decay[i], mult[i])
+    for p, r in zip(ps, ref_p):
+        np.testing.assert_allclose(p.value.numpy(), r, atol=1e-12)
+        assert float(p.grad.abs().sum()) == 0.0
