@@ -363,33 +363,50 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
       const float* pxa = xa + 2 * fm.jsp;
       const float* pxb = p.x + rb * p.ldx + 2 * fm.jsp;
       const float* pa = p.a + 2 * fm.jsp;
+      // All x / a loads of the row pair are issued before any store or
+      // volatile index load, so their L2 latencies overlap instead of
+      // serialising once per q.
+      float2 xav[8], xbv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        xav[q] = ld_f2(pxa + 2 * q * S);
+        xbv[q] = ld_f2(pxb + 2 * q * S);  // row rb == ra when !hasb: in bounds, unused
+      }
+      const bool relu = p.epi_relu;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const float2 av = ld_f2(pa + 2 * q * S);
-        const float2 xav = ld_f2(pxa + 2 * q * S);
-        const float2 xbv = hasb ? ld_f2(pxb + 2 * q * S) : make_float2(0.f, 0.f);
-        st_ga[(2 * q) * T] += fmaf(gb[q].x, xbv.x, ga[q].x * xav.x);
-        st_ga[(2 * q + 1) * T] += fmaf(gb[q].y, xbv.y, ga[q].y * xav.y);
+        if (!hasb) xbv[q] = make_float2(0.f, 0.f);
+        st_ga[(2 * q) * T] += fmaf(gb[q].x, xbv[q].x, ga[q].x * xav[q].x);
+        st_ga[(2 * q + 1) * T] += fmaf(gb[q].y, xbv[q].y, ga[q].y * xav[q].y);
         float2 da = make_float2(av.x * ga[q].x, av.y * ga[q].y);
         float2 db = make_float2(av.x * gb[q].x, av.y * gb[q].y);
-        if (p.epi_relu) {  // previous block's ReLU: mask = x > 0 (layers.py:227, 233)
-          da = make_float2(xav.x > 0.f ? da.x : 0.f, xav.y > 0.f ? da.y : 0.f);
-          db = make_float2(xbv.x > 0.f ? db.x : 0.f, xbv.y > 0.f ? db.y : 0.f);
+        if (relu) {  // previous block's ReLU: mask = x > 0 (layers.py:227, 233)
+          da = make_float2(xav[q].x > 0.f ? da.x : 0.f, xav[q].y > 0.f ? da.y : 0.f);
+          db = make_float2(xbv[q].x > 0.f ? db.x : 0.f, xbv[q].y > 0.f ? db.y : 0.f);
         }
-        if (p.epi_perm) {  // previous block's permutation: out[perm[j]] = g[j] (layers.py:263-265)
+        ga[q] = da;
+        gb[q] = db;
+      }
+      if (p.epi_perm) {  // previous block's permutation: out[perm[j]] = g[j] (layers.py:263-265)
+        float* ra_ = p.y + ra * p.ldo;
+        float* rb_ = p.y + rb * p.ldo;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
           const int* pp = p.epi_perm + 2 * (fm.jsp + q * S);
           const int j0 = ld_plain_i(pp), j1 = ld_plain_i(pp + 1);
-          float* ra_ = p.y + ra * p.ldo;
-          float* rb_ = p.y + rb * p.ldo;
-          ra_[j0] = da.x;
-          ra_[j1] = da.y;
+          ra_[j0] = ga[q].x;
+          ra_[j1] = ga[q].y;
           if (hasb) {
-            rb_[j0] = db.x;
-            rb_[j1] = db.y;
+            rb_[j0] = gb[q].x;
+            rb_[j1] = gb[q].y;
           }
-        } else {
-          oa[q * S] = da;
-          if (hasb) ob[q * S] = db;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          oa[q * S] = ga[q];
+          if (hasb) ob[q * S] = gb[q];
         }
       }
     }
