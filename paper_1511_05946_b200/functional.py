@@ -380,26 +380,62 @@ class HostPipeline:
     writes them back to host, and accumulates the parameter gradients into
     ``grads`` (device, summed over all chunks: the reference's "+=" semantics).
     Chunks are independent rows, so the result equals one full-batch call.
+
+    ``direct_out``: the kernels store y and dx straight into the pinned host
+    buffers (mapped through unified addressing: posted PCIe writes from the
+    SMs), so there is no device->host copy stage to schedule around.
     """
 
-    def __init__(self, n: int, rows: int, device, chunks: int = 8, h2cache: bool = True):
+    def __init__(self, n: int, rows: int, device, chunks: int = 8, h2cache: bool = True, nbuf: int = 2,
+                 ramp: bool = False, direct_out: bool = False):
         self.n, self.rows, self.dev = n, rows, torch.device(device)
-        self.chunks = max(1, min(chunks, rows))
-        bounds = torch.linspace(0, rows, self.chunks + 1).long().tolist()
-        self.spans = [(bounds[i], bounds[i + 1]) for i in range(self.chunks) if bounds[i + 1] > bounds[i]]
+        self.direct_out = direct_out
+        self.spans = self.plan(rows, chunks, ramp)
+        self.chunks = len(self.spans)
         mx = max(b - a for a, b in self.spans)
-        # two device buffer sets so chunk i+1 uploads while chunk i computes
-        self.xd = [torch.empty(mx, n, device=self.dev) for _ in range(2)]
-        self.dyd = [torch.empty(mx, n, device=self.dev) for _ in range(2)]
-        self.yd = [torch.empty(mx, n, device=self.dev) for _ in range(2)]
-        self.dxd = [torch.empty(mx, n, device=self.dev) for _ in range(2)]
-        self.hc = [new_h2cache(mx, n, self.dev) for _ in range(2)] if (h2cache and h2cache_supported(n)) else None
+        # nbuf device buffer sets: chunk i+1.. upload while chunk i computes / downloads
+        self.nbuf = max(2, nbuf)
+        self.xd = [torch.empty(mx, n, device=self.dev) for _ in range(self.nbuf)]
+        self.dyd = [torch.empty(mx, n, device=self.dev) for _ in range(self.nbuf)]
+        nout = 0 if direct_out else self.nbuf
+        self.yd = [torch.empty(mx, n, device=self.dev) for _ in range(nout)]
+        self.dxd = [torch.empty(mx, n, device=self.dev) for _ in range(nout)]
+        self.hc = ([new_h2cache(mx, n, self.dev) for _ in range(self.nbuf)]
+                   if (h2cache and h2cache_supported(n)) else None)
         self.s_in = torch.cuda.Stream(self.dev)
         self.s_cmp = torch.cuda.Stream(self.dev)
         self.s_out = torch.cuda.Stream(self.dev)
         prepare(n, self.dev)
 
-    def step(self, x_host, dy_host, y_host, dx_host, a, d, bias, grads, accumulate=True):
+    @staticmethod
+    def plan(rows: int, chunks: int, ramp: bool = True):
+        """Row spans.  With ``ramp`` the first and last chunks shrink
+        geometrically (1/8, 1/4, 1/2 of the uniform size): the upload of the
+        first chunk and the download of the last one are the only transfers
+        that cannot overlap a transfer in the other direction."""
+        chunks = max(1, min(chunks, rows))
+        u = -(-rows // chunks)
+        sizes = []
+        if ramp and chunks >= 4 and u >= 16:
+            head = [max(1, u // 8), max(1, u // 4), max(1, u // 2)]
+            tail = head[::-1]
+            mid = rows - sum(head) - sum(tail)
+            if mid > 0:
+                k = max(1, -(-mid // u))
+                base, extra = divmod(mid, k)
+                sizes = head + [base + (1 if i < extra else 0) for i in range(k)] + tail
+        if not sizes:
+            base, extra = divmod(rows, chunks)
+            sizes = [base + (1 if i < extra else 0) for i in range(chunks)]
+        spans, lo = [], 0
+        for m in sizes:
+            if m > 0:
+                spans.append((lo, lo + m))
+                lo += m
+        assert lo == rows
+        return spans
+
+    def step(self, x_host, dy_host, y_host, dx_host, a, d, bias, grads, accumulate=True, timeline=False):
         """All host tensors must be pinned CPU fp32 (rows, n).  Returns after
         enqueueing; call ``torch.cuda.synchronize()`` (or an event) to wait."""
         ga, gd, gb = grads
@@ -408,29 +444,35 @@ class HostPipeline:
                 ga.zero_()
                 gd.zero_()
                 gb.zero_()
-        up = [torch.cuda.Event() for _ in self.spans]
-        done = [torch.cuda.Event() for _ in self.spans]
-        down = [torch.cuda.Event() for _ in self.spans]
+        up = [torch.cuda.Event(enable_timing=timeline) for _ in self.spans]
+        done = [torch.cuda.Event(enable_timing=timeline) for _ in self.spans]
+        down = [torch.cuda.Event(enable_timing=timeline) for _ in self.spans]
         cur = torch.cuda.current_stream(self.dev)
         for s in (self.s_in, self.s_cmp, self.s_out):
             s.wait_stream(cur)
+        nb = self.nbuf
         for i, (lo, hi) in enumerate(self.spans):
-            k, m = i % 2, hi - lo
+            k, m = i % nb, hi - lo
             with torch.cuda.stream(self.s_in):
-                if i >= 2:  # buffer set k is free once chunk i-2 was computed
-                    self.s_in.wait_event(done[i - 2])
+                if i >= nb:  # buffer set k is free once chunk i-nb was computed
+                    self.s_in.wait_event(done[i - nb])
                 self.xd[k][:m].copy_(x_host[lo:hi], non_blocking=True)
                 self.dyd[k][:m].copy_(dy_host[lo:hi], non_blocking=True)
                 up[i].record(self.s_in)
             with torch.cuda.stream(self.s_cmp):
                 self.s_cmp.wait_event(up[i])
-                if i >= 2:  # outputs of chunk i-2 must be downloaded first
-                    self.s_cmp.wait_event(down[i - 2])
+                if i >= nb and not self.direct_out:  # outputs of chunk i-nb must be downloaded first
+                    self.s_cmp.wait_event(down[i - nb])
                 hc = self.hc[k] if self.hc is not None else None
-                acdc_forward(self.xd[k][:m], a, d, bias, out=self.yd[k][:m], h2cache=hc)
-                acdc_backward(self.xd[k][:m], self.dyd[k][:m], a, d, ga, gd, gb, accumulate=True,
-                              out=self.dxd[k][:m], h2cache=hc)
+                yo = y_host[lo:hi] if self.direct_out else self.yd[k][:m]
+                dxo = dx_host[lo:hi] if self.direct_out else self.dxd[k][:m]
+                acdc_forward(self.xd[k][:m], a, d, bias, out=yo, h2cache=hc)
+                acdc_backward(self.xd[k][:m], self.dyd[k][:m], a, d, ga, gd, gb, accumulate=True, out=dxo,
+                              h2cache=hc)
                 done[i].record(self.s_cmp)
+            if self.direct_out:
+                down[i] = done[i]
+                continue
             with torch.cuda.stream(self.s_out):
                 self.s_out.wait_event(done[i])
                 y_host[lo:hi].copy_(self.yd[k][:m], non_blocking=True)
@@ -438,3 +480,5 @@ class HostPipeline:
                 down[i].record(self.s_out)
         for s in (self.s_in, self.s_cmp, self.s_out):
             cur.wait_stream(s)
+        if timeline:  # (upload, compute, download) completion events per chunk
+            return list(zip(up, done, down))
