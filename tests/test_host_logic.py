@@ -1,0 +1,23 @@
+"""Host-side logic that needs no GPU: the HostPipeline chunk plan."""
+
+import pytest
+
+from paper_1511_05946_b200.functional import HostPipeline
+
+
+@pytest.mark.parametrize("rows", [1, 2, 5, 63, 64, 100, 1000, 16384, 16385])
+@pytest.mark.parametrize("chunks", [1, 3, 8, 16, 64])
+@pytest.mark.parametrize("ramp", [False, True])
+def test_chunk_plan_partitions_rows(rows, chunks, ramp):
+    spans = HostPipeline.plan(rows, chunks, ramp)
+    assert spans[0][0] == 0 and spans[-1][1] == rows
+    assert all(hi > lo for lo, hi in spans)
+    assert all(spans[i][1] == spans[i + 1][0] for i in range(len(spans) - 1))
+    if not ramp:
+        assert len(spans) == min(chunks, rows)
+
+
+def test_chunk_plan_ramp_shrinks_ends():
+    sizes = [hi - lo for lo, hi in HostPipeline.plan(16384, 16, True)]
+    assert sizes[0] < sizes[1] < sizes[2] < sizes[3]
+    assert sizes[-1] < sizes[-2] < sizes[-3] < sizes[-4]

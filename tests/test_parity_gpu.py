@@ -244,15 +244,18 @@ def test_h2cache_matches_recompute(n, rows):
         F.new_h2cache(4, 128, DEV)
 
 
-def test_host_pipeline_matches_device_path():
-    """functional.HostPipeline (chunked H2D / kernels / D2H overlap) == one device call."""
+@pytest.mark.parametrize("chunks,nbuf,ramp,direct", [(5, 2, False, False), (16, 3, True, False), (7, 2, False, True)])
+def test_host_pipeline_matches_device_path(chunks, nbuf, ramp, direct):
+    """functional.HostPipeline (chunked H2D / kernels / D2H overlap, or kernels
+    storing straight into mapped host memory) == one device call."""
     from paper_1511_05946_b200 import functional as F
 
     n, rows = 1024, 300
     rng = np.random.default_rng(21)
     x, dy = f32(rng, rows, n), f32(rng, rows, n)
     a, d, b = (t32(f32(rng, n, mean=m, std=0.3)) for m in (1.0, 1.0, 0.0))
-    pipe = F.HostPipeline(n, rows, DEV, chunks=5)
+    pipe = F.HostPipeline(n, rows, DEV, chunks=chunks, nbuf=nbuf, ramp=ramp, direct_out=direct)
+    assert sum(hi - lo for lo, hi in pipe.spans) == rows
     xh, dyh = torch.as_tensor(x).pin_memory(), torch.as_tensor(dy).pin_memory()
     yh, dxh = torch.empty(rows, n).pin_memory(), torch.empty(rows, n).pin_memory()
     g = [torch.zeros(n, device=DEV) for _ in range(3)]
