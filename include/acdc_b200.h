@@ -27,6 +27,8 @@
  *   acdc_prepare   DctPlan(n, mode="fast") table build transforms.py:86-122
  *   afdf_fwd_c64   AfdfLayer.forward                 layers.py:199-204
  *   afdf_bwd_c64   AfdfLayer.backward (accumulates)  layers.py:206-215
+ *   acdc_fft_c64   fft(plan, z) / ifft(plan, z) / kernels.fft_inplace
+ *                                                    transforms.py:166-179, _kernels.pyx:18-57
  */
 #ifndef ACDC_B200_H
 #define ACDC_B200_H
@@ -133,6 +135,14 @@ size_t afdf_bwd_workspace_bytes(int64_t rows, int32_t n);
 int afdf_bwd_c64(const float* x, const float* dy, float* dx, const float* a, const float* d, float* grad_a,
                  float* grad_d, int accumulate, void* ws, size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx,
                  int64_t ldy, int64_t lddx, acdc_stream_t stream);
+
+/* Row-wise complex DFT of interleaved complex64 rows (transforms.py:166-179,
+ * _kernels.pyx:18-57): inverse == 0: out = FFT(z) (unnormalised);
+ * inverse != 0: out = IFFT(z) = conj(FFT(conj z)) / n.  z == out (in place)
+ * is allowed; ldz, ldo in complex elements.  Non-power-of-two n gives
+ * ACDC_E_SIZE with FftPlan's message (transforms.py:77-78). */
+int acdc_fft_c64(const float* z, float* out, int64_t rows, int32_t n, int inverse, int64_t ldz, int64_t ldo,
+                 acdc_stream_t stream);
 
 #ifdef __cplusplus
 }

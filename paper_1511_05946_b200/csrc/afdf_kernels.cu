@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "fft_engine.cuh"
 #include "runtime.h"
@@ -122,6 +123,44 @@ __global__ void ACDC_LB(Geo<LOGN>) afdf_fwd_kernel(FParams p) {
       for (int q = 0; q < RL; ++q) {
         const float2 h = v[b * RL + q];
         yr[fpos<G, PL>(b, q)] = make_float2(h.x * scale, -h.y * scale);
+      }
+  }
+}
+
+// Row-wise complex DFT (transforms.py:166-179, _kernels.pyx:18-57): forward
+// unnormalised, inverse = conj(FFT(conj z)) / N.  Reads a whole row into
+// registers before writing, so z == out (in place) is allowed.
+template <int LOGN, bool INV>
+__global__ void ACDC_LB(Geo<LOGN>) fft_rows_kernel(FParams p) {
+  using G = Geo<LOGN>;
+  constexpr int E = G::E;
+  constexpr int R0 = G::radix(0), PL = G::NPASS - 1, RL = G::radix(PL);
+  extern __shared__ __align__(16) float smem_f[];
+  const int grp = threadIdx.x / G::T, t = threadIdx.x % G::T;
+  const int64_t gid = (int64_t)blockIdx.x * G::GPC + grp, gstride = (int64_t)gridDim.x * G::GPC;
+  GroupSync<G> gs(grp);
+  Xbuf<G> xb{smem_f + G::TAB_FLOATS + grp * G::GROUP_FLOATS, 0};
+  const float2* tw;
+  f_stage_tables<G>(p, smem_f, tw);
+  const float scale = 1.0f / G::N;
+  for (int64_t r = gid; r < p.rows; r += gstride) {
+    const float2* xr = p.x + r * p.ldx + t;
+    float2 v[E];
+#pragma unroll
+    for (int b = 0; b < E / R0; ++b)
+#pragma unroll
+      for (int q = 0; q < R0; ++q) {
+        const float2 z = ld_param(xr + fpos<G, 0>(b, q));
+        v[b * R0 + q] = INV ? conjf2(z) : z;
+      }
+    fft_passes<G>(v, xb, gs, tw, t);
+    float2* yr = p.y + r * p.ldo + t;
+#pragma unroll
+    for (int b = 0; b < E / RL; ++b)
+#pragma unroll
+      for (int q = 0; q < RL; ++q) {
+        const float2 h = v[b * RL + q];
+        yr[fpos<G, PL>(b, q)] = INV ? make_float2(h.x * scale, -h.y * scale) : h;
       }
   }
 }
@@ -247,12 +286,17 @@ __global__ void __launch_bounds__(256) afdf_grad_reduce_kernel(const float* __re
   }
 }
 
+// kind: 0 = AFDF forward, 1 = AFDF backward, 2 = FFT rows, 3 = inverse FFT rows
 template <int LOGN>
-static LaunchInfo finfo(bool bwd) {
+static LaunchInfo finfo(int kind) {
   using G = Geo<LOGN>;
   using GB = GeoF<LOGN>;
+  const bool bwd = kind == 1;
   LaunchInfo li;
-  li.fn = bwd ? (const void*)afdf_bwd_kernel<LOGN> : (const void*)afdf_fwd_kernel<LOGN>;
+  li.fn = kind == 0   ? (const void*)afdf_fwd_kernel<LOGN>
+          : kind == 1 ? (const void*)afdf_bwd_kernel<LOGN>
+          : kind == 2 ? (const void*)fft_rows_kernel<LOGN, false>
+                      : (const void*)fft_rows_kernel<LOGN, true>;
   li.cta = G::CTA;
   li.gpc = G::GPC;
   li.scratch = bwd ? GB::GSCRATCH_FLOATS : 0;
@@ -260,11 +304,47 @@ static LaunchInfo finfo(bool bwd) {
   return li;
 }
 
+template <int LOGN>
+static LaunchInfo finfo_fft(bool inverse) {
+  return finfo<LOGN>(inverse ? 3 : 2);
+}
+
+static int fft_info_for(int logn, bool inverse, LaunchInfo* li) {
+  switch (logn) {
+#define ACDC_TCASE(L)               \
+  case L:                           \
+    *li = finfo_fft<L>(inverse);    \
+    return ACDC_OK;
+#ifndef ACDC_ONLY_LOGN
+    ACDC_TCASE(1)
+    ACDC_TCASE(2)
+    ACDC_TCASE(3)
+    ACDC_TCASE(4)
+    ACDC_TCASE(5)
+    ACDC_TCASE(6)
+    ACDC_TCASE(7)
+    ACDC_TCASE(8)
+    ACDC_TCASE(9)
+    ACDC_TCASE(10)
+    ACDC_TCASE(11)
+    ACDC_TCASE(12)
+    ACDC_TCASE(13)
+    ACDC_TCASE(14)
+    ACDC_TCASE(15)
+#else
+    ACDC_TCASE(ACDC_ONLY_LOGN)
+#endif
+#undef ACDC_TCASE
+    default:
+      return set_error(ACDC_E_SIZE, "FFT rows support power-of-two sizes 1..32768");
+  }
+}
+
 static int finfo_for(int logn, bool bwd, LaunchInfo* li) {
   switch (logn) {
 #define ACDC_FCASE(L)       \
   case L:                   \
-    *li = finfo<L>(bwd);    \
+    *li = finfo<L>(bwd ? 1 : 0);    \
     return ACDC_OK;
 #ifndef ACDC_ONLY_LOGN
     ACDC_FCASE(1)
@@ -383,6 +463,43 @@ int afdf_bwd_c64(const float* x, const float* dy, float* dx, const float* a, con
                                                                      accumulate);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
+}
+
+int acdc_fft_c64(const float* z, float* out, int64_t rows, int32_t n, int inverse, int64_t ldz, int64_t ldo,
+                 acdc_stream_t stream) {
+  if (n < 1 || (n & (n - 1)) != 0) {  // FftPlan's message (transforms.py:77-78)
+    char msg[96];
+    snprintf(msg, sizeof(msg), "FFT size must be a power of two, got %d", n);
+    return set_error(ACDC_E_SIZE, msg);
+  }
+  int logn;
+  int rc = check_n(n, &logn);
+  if (rc) return rc;
+  if (rows < 0 || ldz < n || ldo < n) return ACDC_E_SHAPE;
+  if (rows > 0 && (!z || !out)) return ACDC_E_NULL;
+  if (((uintptr_t)z | (uintptr_t)out) & 7) return ACDC_E_ALIGN;
+  if (rows == 0) return ACDC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (logn == 0) {  // the 1-point DFT (and its inverse) is the identity
+    if (z == out) return ACDC_OK;
+    cudaError_t e = cudaMemcpy2DAsync(out, 8 * (size_t)ldo, z, 8 * (size_t)ldz, 8, (size_t)rows,
+                                      cudaMemcpyDeviceToDevice, st);
+    return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
+  }
+  Tables tb;
+  if ((rc = get_tables(logn, &tb))) return rc;
+  LaunchInfo li;
+  if ((rc = fft_info_for(logn, inverse != 0, &li))) return rc;
+  int64_t grid;
+  if ((rc = grid_for(li, rows, &grid))) return rc;
+  FParams p{};
+  p.x = (const float2*)z;
+  p.y = (float2*)out;
+  p.tab = tb.tab;
+  p.rows = rows;
+  p.ldx = ldz;
+  p.ldo = ldo;
+  return launch(li, grid, &p, st);
 }
 
 }  // extern "C"

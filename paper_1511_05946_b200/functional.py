@@ -20,6 +20,8 @@ __all__ = [
     "acdc_forward",
     "acdc_backward",
     "dct",
+    "fft",
+    "ifft",
     "idct",
     "AcdcFunction",
     "acdc",
@@ -181,6 +183,35 @@ def dct(x: torch.Tensor) -> torch.Tensor:
 def idct(x: torch.Tensor) -> torch.Tensor:
     """Row-wise orthonormal DCT-III, the inverse of :func:`dct` (transforms.py:148-156)."""
     return _transform("acdc_dct3_f32", x)
+
+
+def _fft_rows(z: torch.Tensor, inverse: bool, out: torch.Tensor | None = None) -> torch.Tensor:
+    squeeze = z.dim() == 1
+    if squeeze:
+        z = z.unsqueeze(0)
+    if not isinstance(z, torch.Tensor) or not z.is_cuda or z.dim() != 2:
+        raise ValueError("expected a 1-D or 2-D CUDA tensor")
+    if z.dtype != torch.complex64:
+        z = z.to(torch.complex64)
+    if z.stride(1) != 1 or (z.shape[0] > 1 and z.stride(0) < z.shape[1]):
+        z = z.contiguous()
+    n = z.shape[1]
+    y = torch.empty_like(z, memory_format=torch.contiguous_format) if out is None else out
+    lib = _lib.load()
+    with torch.cuda.device(z.device):
+        _lib.check(lib.acdc_fft_c64(_ptr(z), _ptr(y), z.shape[0], n, 1 if inverse else 0, _ld(z, n), _ld(y, n),
+                                    _stream(z)))
+    return y[0] if squeeze else y
+
+
+def fft(z: torch.Tensor) -> torch.Tensor:
+    """Unnormalised forward DFT of each complex64 row (transforms.py:166-171)."""
+    return _fft_rows(z, False)
+
+
+def ifft(z: torch.Tensor) -> torch.Tensor:
+    """Inverse DFT of each complex64 row, scaled by 1/N (transforms.py:174-179)."""
+    return _fft_rows(z, True)
 
 
 class AcdcFunction(torch.autograd.Function):

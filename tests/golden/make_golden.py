@@ -13,6 +13,7 @@ then up-cast) so the same inputs feed the fp32 CUDA kernels in the GPU tests.
 
 Cases (keys prefixed per case):
   dct_N*:   dct / idct of a (3, N) batch, N in {1,2,4,...,1024}   (transforms.py:137-156)
+  fft_N*:   fft / ifft of a (3, N) complex batch, N in {1,...,4096} (transforms.py:166-179)
   acdc_*:   AcdcLayer forward, backward twice (accumulation)        (layers.py:141-156)
   afdf_*:   AfdfLayer forward/backward, complex                     (layers.py:199-215)
   casc_*:   Cascade of ACDC / ReLU / Permutation                    (layers.py:336-344)
@@ -132,6 +133,16 @@ def main():
     z.a[:] = 0.0
     z.bias_d[:] = f32(rng, n)
     out["ka_a0_bias"], out["ka_a0_y"] = z.bias_d.copy(), z.forward(x)
+
+    # fft_N*: fft / ifft of a (3, N) complex batch (transforms.py:166-179);
+    # own generator so the arrays above keep their values
+    frng = np.random.default_rng(20261017)
+    for n in [1, 2, 4, 8, 16, 32, 64, 128, 256, 1024, 4096]:
+        plan = acdc.FftPlan(n, backend="compiled")
+        z = f32(frng, 3, n) + 1j * f32(frng, 3, n)
+        out[f"fft_N{n}_z"] = z
+        out[f"fft_N{n}_fft"] = acdc.fft(plan, z)
+        out[f"fft_N{n}_ifft"] = acdc.ifft(plan, z)
 
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
     np.savez_compressed(path, **out)

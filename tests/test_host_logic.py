@@ -21,3 +21,19 @@ def test_chunk_plan_ramp_shrinks_ends():
     sizes = [hi - lo for lo, hi in HostPipeline.plan(16384, 16, True)]
     assert sizes[0] < sizes[1] < sizes[2] < sizes[3]
     assert sizes[-1] < sizes[-2] < sizes[-3] < sizes[-4]
+
+
+def test_kernel_plugin_matches_reference_signatures():
+    """kernels_b200 exposes the kernel-module interface get_kernels returns
+    (backend.py:30-42): COMPILED and the _kernels.pyx:49-91 signatures."""
+    import inspect
+
+    from paper_1511_05946_b200 import kernels_b200 as K
+
+    assert K.COMPILED is True
+    sig = {name: list(inspect.signature(getattr(K, name)).parameters) for name in K.__all__ if name != "COMPILED"}
+    assert sig == {
+        "fft_inplace": ["z", "rev", "tw", "inverse"],
+        "dct2_batch": ["x", "out", "reorder", "rev", "tw", "w4s"],
+        "dct3_batch": ["y", "out", "reorder", "rev", "tw", "u1", "u2"],
+    }

@@ -23,6 +23,15 @@ def test_dct_matches_reference(golden):
         np.testing.assert_allclose(O.dct3_rows(x), golden[p + "_idct"], atol=1e-13, rtol=0)
 
 
+def test_fft_matches_reference(golden):
+    ns = sorted({int(k.split("_")[1][1:]) for k in golden.files if k.startswith("fft_N")})
+    assert len(ns) >= 10
+    for n in ns:
+        z = golden[f"fft_N{n}_z"]
+        np.testing.assert_allclose(O.fft_rows(z), golden[f"fft_N{n}_fft"], atol=1e-12, rtol=0)
+        np.testing.assert_allclose(O.ifft_rows(z), golden[f"fft_N{n}_ifft"], atol=1e-13, rtol=0)
+
+
 def test_dct_matches_naive_matrix():
     rng = np.random.default_rng(0)
     for n in [1, 2, 8, 64, 1024]:
