@@ -458,13 +458,18 @@ class HostPipeline:
         if not sizes:
             base, extra = divmod(rows, chunks)
             sizes = [base + (1 if i < extra else 0) for i in range(chunks)]
-        spans, lo = [], 0
+        # interior boundaries even: the kernels pack rows (2k, 2k+1) into one
+        # complex FFT, so even chunk starts keep the full-batch pairing and
+        # y / dx bit-identical to one call over all rows
+        bounds, lo = [0], 0
         for m in sizes:
-            if m > 0:
-                spans.append((lo, lo + m))
-                lo += m
-        assert lo == rows
-        return spans
+            lo += m
+            b = rows if lo >= rows else lo & ~1
+            if b > bounds[-1]:
+                bounds.append(b)
+        if bounds[-1] != rows:
+            bounds.append(rows)
+        return [(bounds[i], bounds[i + 1]) for i in range(len(bounds) - 1)]
 
     def step(self, x_host, dy_host, y_host, dx_host, a, d, bias, grads, accumulate=True, timeline=False):
         """All host tensors must be pinned CPU fp32 (rows, n).  Returns after

@@ -13,8 +13,8 @@ def test_chunk_plan_partitions_rows(rows, chunks, ramp):
     assert spans[0][0] == 0 and spans[-1][1] == rows
     assert all(hi > lo for lo, hi in spans)
     assert all(spans[i][1] == spans[i + 1][0] for i in range(len(spans) - 1))
-    if not ramp:
-        assert len(spans) == min(chunks, rows)
+    assert all(lo % 2 == 0 for lo, _ in spans)  # row pairs never split across chunks
+    assert len(spans) <= max(chunks, 1) + 6
 
 
 def test_chunk_plan_ramp_shrinks_ends():
