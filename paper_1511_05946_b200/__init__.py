@@ -32,6 +32,8 @@ from .layers import (
     acdc_cascade,
     afdf_cascade,
     count_params,
+    load_cascade,
+    save_cascade,
 )
 
 __version__ = "0.1.0"

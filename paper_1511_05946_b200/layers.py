@@ -12,11 +12,17 @@ sm_100a kernels (``functional.py`` -> ``libacdc_b200.so``), in fp32.
   accumulates into the gradients (layers.py:152-155) until ``zero_grads``.
 * ``backward`` before ``forward`` raises ``RuntimeError`` and consumes the
   cache unless ``retain_cache`` (layers.py:99-105).
-* The layer caches only ``x``; ``h2`` is recomputed inside the fused backward
-  kernel instead of being stored (layers.py:145).
+* Like the reference (layers.py:145), ``AcdcLayer`` caches ``x`` and
+  ``h2 = C2(a * x)`` (in the kernels' native layout) on the sizes that support
+  it (256 <= N <= 16384); elsewhere, or with ``cache_h2=False``, the backward
+  kernel recomputes h2.
+* ``save_cascade`` / ``load_cascade`` read and write the reference's JSON
+  format (layers.py:466-554, format version 1).
 """
 
 from __future__ import annotations
+
+import json
 
 from dataclasses import dataclass
 
@@ -37,7 +43,12 @@ __all__ = [
     "acdc_cascade",
     "afdf_cascade",
     "count_params",
+    "save_cascade",
+    "load_cascade",
+    "FORMAT_VERSION",
 ]
+
+FORMAT_VERSION = 1  # layers.py:47
 
 
 def _is_pow2(n: int) -> bool:
@@ -122,6 +133,16 @@ class Layer:
         return y.detach().to("cpu", dtype=dt).numpy()
 
 
+@dataclass(frozen=True)
+class DctPlanInfo:
+    """What ``AcdcLayer.dct_plan`` exposes of the reference plan (transforms.py:86-95):
+    size, mode and backend; the tables themselves live in the CUDA library."""
+
+    n: int
+    mode: str
+    backend: str
+
+
 class AcdcLayer(Layer):
     """Diagonal, DCT, diagonal-with-bias, inverse DCT (layers.py:108-156).
 
@@ -130,7 +151,7 @@ class AcdcLayer(Layer):
     is accepted for API parity and computes the same orthonormal transform.
     """
 
-    def __init__(self, n, dct_mode="fast", backend="auto", device=None):
+    def __init__(self, n, dct_mode="fast", backend="auto", device=None, cache_h2=True):
         if dct_mode not in ("naive", "fast"):
             raise ValueError(f"unknown DCT mode {dct_mode!r}, expected one of ('naive', 'fast')")
         if not _is_pow2(n):
@@ -138,6 +159,8 @@ class AcdcLayer(Layer):
         self.n_in = self.n_out = n
         self.dct_mode = dct_mode
         self.backend = backend
+        self.dct_plan = DctPlanInfo(n, dct_mode, "b200")
+        self.cache_h2 = bool(cache_h2) and F.h2cache_supported(n)
         self.device = _device(device)
         kw = dict(dtype=torch.float32, device=self.device)
         self.a = torch.ones(n, **kw)
@@ -166,16 +189,18 @@ class AcdcLayer(Layer):
 
     def forward(self, x):
         x, host = self._check_input(x)
-        y = F.acdc_forward(x, self.a, self.d, self.bias_d)
-        self._cache = x
+        hc = F.new_h2cache(x.shape[0], self.n_in, self.device) if (self.cache_h2 and x.shape[0]) else None
+        y = F.acdc_forward(x, self.a, self.d, self.bias_d, h2cache=hc)
+        self._cache = (x, hc)
         return self._out(y, host)
 
     def backward(self, grad_y, retain_cache=False):
-        x = self._take_cache(retain_cache)
+        x, hc = self._take_cache(retain_cache)
         gy, host = self._check_input(grad_y)
         if gy.shape[0] != x.shape[0]:
             raise ValueError(f"grad_y has {gy.shape[0]} rows, forward input had {x.shape[0]}")
-        dx = F.acdc_backward(x, gy, self.a, self.d, self.grad_a, self.grad_d, self.grad_bias_d, accumulate=True)
+        dx = F.acdc_backward(x, gy, self.a, self.d, self.grad_a, self.grad_d, self.grad_bias_d, accumulate=True,
+                             h2cache=hc)
         return self._out(dx, host)
 
 
@@ -276,17 +301,23 @@ class PermutationLayer(Layer):
         self._inv_t = torch.as_tensor(self.inverse_perm, device=self.device)
         self._cache = None
 
+    @staticmethod
+    def _dtype(x):
+        """Dtype-agnostic like the reference (no cast): complex stays complex."""
+        cplx = x.is_complex() if isinstance(x, torch.Tensor) else np.iscomplexobj(x)
+        return torch.complex64 if cplx else torch.float32
+
     def forward(self, x):
         shape = tuple(x.shape) if hasattr(x, "shape") else np.shape(x)
         if shape[1:] != (self.n_in,):
             raise ValueError(f"PermutationLayer expects (batch, {self.n_in}) input")
-        x, host = self._check_input(x)
+        x, host = self._check_input(x, self._dtype(x))
         self._cache = True
         return self._out(x.index_select(1, self._perm_t), host)
 
     def backward(self, grad_y, retain_cache=False):
         self._take_cache(retain_cache)
-        gy, host = self._check_input(grad_y)
+        gy, host = self._check_input(grad_y, self._dtype(grad_y))
         return self._out(gy.index_select(1, self._inv_t), host)
 
 
@@ -465,3 +496,80 @@ def afdf_cascade(n, depth, backend="auto", device=None):
 def count_params(obj):
     """3N per ACDC, 4N per AFDF, N*M+M per dense (layers.py:461-463)."""
     return obj.param_count()
+
+
+# ------------------------------------------------------------ JSON interop
+# The reference's on-disk cascade format (layers.py:466-554): one JSON document
+# {"format_version": 1, "seed": ..., "layers": [spec, ...]} with float64 values.
+# Parameters here are fp32: saving writes their exact values (so a file saved
+# here reloads bit-exactly, here and in the reference); loading a reference
+# file rounds each value to the nearest fp32.
+
+def _tolist(t: torch.Tensor):
+    return t.detach().to("cpu", dtype=torch.float64).tolist()
+
+
+def _layer_spec(layer):
+    if isinstance(layer, AcdcLayer):
+        return {"type": "acdc", "n": layer.n_in, "dct_mode": layer.dct_mode, "a": _tolist(layer.a),
+                "d": _tolist(layer.d), "bias_d": _tolist(layer.bias_d)}
+    if isinstance(layer, AfdfLayer):
+        return {"type": "afdf", "n": layer.n_in, "fix_a": layer.fix_a, "a_re": _tolist(layer.a.real),
+                "a_im": _tolist(layer.a.imag), "d_re": _tolist(layer.d.real), "d_im": _tolist(layer.d.imag)}
+    if isinstance(layer, ReluLayer):
+        return {"type": "relu", "n": layer.n_in}
+    if isinstance(layer, PermutationLayer):
+        return {"type": "permutation", "n": layer.n_in, "perm": layer.perm.tolist()}
+    if isinstance(layer, DenseLayer):
+        return {"type": "dense", "n_in": layer.n_in, "n_out": layer.n_out, "w": _tolist(layer.w.reshape(-1)),
+                "b": _tolist(layer.b)}
+    raise TypeError(f"cannot serialize layer {type(layer).__name__}")
+
+
+def _set(dst: torch.Tensor, values):
+    dst.copy_(torch.as_tensor(np.asarray(values, dtype=np.float64).reshape(tuple(dst.shape))).to(dst.dtype))
+
+
+def _layer_from_spec(spec, backend, device):
+    tag = spec["type"]
+    if tag == "acdc":
+        layer = AcdcLayer(spec["n"], dct_mode=spec["dct_mode"], backend=backend, device=device)
+        _set(layer.a, spec["a"])
+        _set(layer.d, spec["d"])
+        _set(layer.bias_d, spec["bias_d"])
+        return layer
+    if tag == "afdf":
+        layer = AfdfLayer(spec["n"], backend=backend, fix_a=spec["fix_a"], device=device)
+        a = np.asarray(spec["a_re"], dtype=np.float64) + 1j * np.asarray(spec["a_im"], dtype=np.float64)
+        d = np.asarray(spec["d_re"], dtype=np.float64) + 1j * np.asarray(spec["d_im"], dtype=np.float64)
+        layer.a.copy_(torch.as_tensor(a).to(torch.complex64))
+        layer.d.copy_(torch.as_tensor(d).to(torch.complex64))
+        return layer
+    if tag == "relu":
+        return ReluLayer(spec["n"], device=device)
+    if tag == "permutation":
+        return PermutationLayer(spec["n"], perm=spec["perm"], device=device)
+    if tag == "dense":
+        layer = DenseLayer(spec["n_in"], spec["n_out"], device=device)
+        _set(layer.w, spec["w"])
+        _set(layer.b, spec["b"])
+        return layer
+    raise ValueError(f"unknown layer tag {tag!r}")
+
+
+def save_cascade(cascade, path, seed=None):
+    """Write a cascade as the reference's JSON document (layers.py:536-545)."""
+    doc = {"format_version": FORMAT_VERSION, "seed": seed, "layers": [_layer_spec(l) for l in cascade.layers]}
+    with open(path, "w", encoding="utf-8") as fh:
+        json.dump(doc, fh)
+        fh.write("\n")
+
+
+def load_cascade(path, backend="auto", device=None):
+    """Read a reference (or ``save_cascade``) JSON file into GPU layers (layers.py:548-554)."""
+    with open(path, "r", encoding="utf-8") as fh:
+        doc = json.load(fh)
+    version = doc.get("format_version")
+    if version != FORMAT_VERSION:
+        raise ValueError(f"unsupported cascade format version {version!r}")
+    return Cascade([_layer_from_spec(s, backend, device) for s in doc["layers"]])

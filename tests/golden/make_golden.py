@@ -14,6 +14,8 @@ then up-cast) so the same inputs feed the fp32 CUDA kernels in the GPU tests.
 Cases (keys prefixed per case):
   dct_N*:   dct / idct of a (3, N) batch, N in {1,2,4,...,1024}   (transforms.py:137-156)
   fft_N*:   fft / ifft of a (3, N) complex batch, N in {1,...,4096} (transforms.py:166-179)
+  json_*:   reference save_cascade files cascade_{real,complex}.json (layers.py:536-554)
+            and the reference forward of a batch through each
   acdc_*:   AcdcLayer forward, backward twice (accumulation)        (layers.py:141-156)
   afdf_*:   AfdfLayer forward/backward, complex                     (layers.py:199-215)
   casc_*:   Cascade of ACDC / ReLU / Permutation                    (layers.py:336-344)
@@ -143,6 +145,34 @@ def main():
         out[f"fft_N{n}_z"] = z
         out[f"fft_N{n}_fft"] = acdc.fft(plan, z)
         out[f"fft_N{n}_ifft"] = acdc.ifft(plan, z)
+
+    # json_*: cascades written by the reference's save_cascade (layers.py:536-545)
+    # with fp32-representable parameters, plus the reference forward of a batch
+    here = os.path.dirname(os.path.abspath(__file__))
+    jrng = np.random.default_rng(20261018)
+    n = 16
+    l0 = acdc.AcdcLayer(n)
+    l3 = acdc.AcdcLayer(n)
+    for L in (l0, l3):
+        L.a[:] = f32(jrng, n, mean=1.0, std=0.3)
+        L.d[:] = f32(jrng, n, mean=1.0, std=0.3)
+        L.bias_d[:] = f32(jrng, n, std=0.2)
+    dense = acdc.DenseLayer(n, 8)
+    dense.w[...] = f32(jrng, n, 8, std=0.3)
+    dense.b[:] = f32(jrng, 8, std=0.1)
+    real = acdc.Cascade([l0, acdc.ReluLayer(n), acdc.PermutationLayer(n, rng=acdc.Rng(5)), l3, dense])
+    acdc.save_cascade(real, os.path.join(here, "cascade_real.json"), seed=5)
+    x = f32(jrng, 4, n)
+    out["json_real_x"], out["json_real_y"] = x, real.forward(x)
+    f0 = acdc.AfdfLayer(n, fix_a=True)
+    f2 = acdc.AfdfLayer(n)
+    for L in (f0, f2):
+        L.a[:] = f32(jrng, n, mean=1.0, std=0.2) + 1j * f32(jrng, n, std=0.2)
+        L.d[:] = f32(jrng, n, mean=1.0, std=0.2) + 1j * f32(jrng, n, std=0.2)
+    cplx = acdc.Cascade([f0, acdc.PermutationLayer(n, rng=acdc.Rng(6)), f2])
+    acdc.save_cascade(cplx, os.path.join(here, "cascade_complex.json"))
+    z = f32(jrng, 4, n) + 1j * f32(jrng, 4, n)
+    out["json_cplx_x"], out["json_cplx_y"] = z, cplx.forward(z)
 
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
     np.savez_compressed(path, **out)

@@ -37,3 +37,28 @@ def test_kernel_plugin_matches_reference_signatures():
         "dct2_batch": ["x", "out", "reorder", "rev", "tw", "w4s"],
         "dct3_batch": ["y", "out", "reorder", "rev", "tw", "u1", "u2"],
     }
+
+
+def test_load_cascade_rejects_other_format_versions(tmp_path):
+    """layers.py:548-553: the version check runs before any layer is built."""
+    import json
+
+    from paper_1511_05946_b200 import load_cascade
+
+    p = tmp_path / "v2.json"
+    p.write_text(json.dumps({"format_version": 2, "seed": None, "layers": []}))
+    with pytest.raises(ValueError, match="unsupported cascade format version 2"):
+        load_cascade(p)
+
+
+def test_reference_cascade_files_are_format_1():
+    import json
+    import os
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    tags = set()
+    for name in ("cascade_real.json", "cascade_complex.json"):
+        doc = json.load(open(os.path.join(here, name)))
+        assert doc["format_version"] == 1
+        tags |= {s["type"] for s in doc["layers"]}
+    assert tags == {"acdc", "afdf", "relu", "permutation", "dense"}
