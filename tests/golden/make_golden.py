@@ -14,6 +14,7 @@ then up-cast) so the same inputs feed the fp32 CUDA kernels in the GPU tests.
 Cases (keys prefixed per case):
   dct_N*:   dct / idct of a (3, N) batch, N in {1,2,4,...,1024}   (transforms.py:137-156)
   fft_N*:   fft / ifft of a (3, N) complex batch, N in {1,...,4096} (transforms.py:166-179)
+  train_*:  Rng streams, make_regression, losses, a 4-epoch training curve, a divergence step
   json_*:   reference save_cascade files cascade_{real,complex}.json (layers.py:536-554)
             and the reference forward of a batch through each
   acdc_*:   AcdcLayer forward, backward twice (accumulation)        (layers.py:141-156)
@@ -173,6 +174,39 @@ def main():
     acdc.save_cascade(cplx, os.path.join(here, "cascade_complex.json"))
     z = f32(jrng, 4, n) + 1j * f32(jrng, 4, n)
     out["json_cplx_x"], out["json_cplx_y"] = z, cplx.forward(z)
+
+    # train_*: training.py pieces — Rng streams, make_regression, host losses,
+    # a short reference training curve and a divergence step
+    r = acdc.Rng(7)
+    c0, c1 = r.spawn(2)
+    out["train_rng_uniform"] = c0.uniform(3, 4)
+    out["train_rng_gauss"] = c1.gaussian(2, 5, 1.0, 0.3)
+    out["train_rng_perm"] = acdc.Rng(8).permutation(10)
+    ds = acdc.make_regression(3, n_samples=20, n_in=4, n_out=3)
+    out["train_reg_x"], out["train_reg_y"], out["train_reg_w"] = ds.x, ds.y, ds.w_true
+    lrng = np.random.default_rng(5)
+    p_, t_ = lrng.standard_normal((4, 6)), lrng.standard_normal((4, 6))
+    out["train_mse_in"] = np.stack([p_, t_])
+    out["train_mse_loss"], out["train_mse_grad"] = np.float64(acdc.mse_loss(p_, t_)[0]), acdc.mse_loss(p_, t_)[1]
+    labels = np.array([0, 5, 2, 3])
+    out["train_ce_labels"] = labels
+    out["train_ce_loss"], out["train_ce_grad"] = (np.float64(acdc.softmax_cross_entropy(p_, labels)[0]),
+                                                  acdc.softmax_cross_entropy(p_, labels)[1])
+    ds = acdc.make_regression(11, n_samples=256, n_in=64, n_out=64)
+    casc = acdc.acdc_cascade(64, 2)
+    cfg = acdc.SgdConfig(learning_rate=0.002, momentum=0.9, lr_decay_factor=0.5, lr_decay_every=12)
+    out["train_curve"] = np.array(acdc.train(casc, ds, cfg, init_scheme=acdc.InitScheme(), epochs=4,
+                                             batch_size=48, seed=1))
+    out["train_curve_params"] = np.stack([np.concatenate([L.a, L.d, L.bias_d]) for L in casc.layers])
+    casc = acdc.acdc_cascade(64, 2)
+    bad_y = ds.y.copy()
+    bad_y[200, 5] = np.nan  # one poisoned target: diverges at the step whose batch holds sample 200
+    try:
+        acdc.train(casc, (ds.x, bad_y), acdc.SgdConfig(learning_rate=0.002, momentum=0.9),
+                   init_scheme=acdc.InitScheme(), epochs=3, batch_size=32, seed=2)
+        out["train_diverge_step"] = np.int64(-1)
+    except acdc.DivergenceError as e:
+        out["train_diverge_step"] = np.int64(e.step)
 
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
     np.savez_compressed(path, **out)
