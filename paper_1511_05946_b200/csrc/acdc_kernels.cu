@@ -207,8 +207,8 @@ __global__ void ACDC_LB(GeoFwd<LOGN>) acdc_fwd_kernel(KParams p) {
             dl = ld_plain(fm.plo(p.d, s)), bl = ld_plain(fm.plo(p.bias, s));
             dh = ld_plain(fm.phi(p.d, s)), bh = ld_plain(fm.phi(p.bias, s));
           }
-          xl = make_float2(fmaf(xl.x, dl, bl), fmaf(xl.y, dl, bl));
-          xh = make_float2(fmaf(xh.x, dh, bh), fmaf(xh.y, dh, bh));
+          xl = vfma(xl, bc(dl), bc(bl));
+          xh = vfma(xh, bc(dh), bc(bh));
           dct3_pre(xl, xh, cs, fm.special(s), chi, gl[s], gh[s]);
         }
         fp_scatter<G>(gl, gh, v, fm);
@@ -244,8 +244,8 @@ __global__ void ACDC_LB(GeoFwd<LOGN>) acdc_fwd_kernel(KParams p) {
     for (int i = 0; i < E / 2; ++i) {
       const float dl = ld_plain(sl.plo(p.d, i)), bl = ld_plain(sl.plo(p.bias, i));
       const float dh = ld_plain(sl.phi(p.d, i)), bh = ld_plain(sl.phi(p.bias, i));
-      X[2 * i] = make_float2(fmaf(X[2 * i].x, dl, bl), fmaf(X[2 * i].y, dl, bl));
-      X[2 * i + 1] = make_float2(fmaf(X[2 * i + 1].x, dh, bh), fmaf(X[2 * i + 1].y, dh, bh));
+      X[2 * i] = vfma(X[2 * i], bc(dl), bc(bl));
+      X[2 * i + 1] = vfma(X[2 * i + 1], bc(dh), bc(bh));
     }
     packed_dct3<G>(X, v, xb, gs, tw, cp, t);
     constexpr int RL = G::radix(PL);
@@ -293,11 +293,17 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
   float* st_ga = sbase + (H2C ? 0 : 2 * E * T) + t;     // [E][T]
   const float2 *tw, *cp;
   stage_tables<G>(p.tab, smem_f, tw, cp);
+  // fast-pairing path: grad_a partials as float2 [q][T] (positions 2m, 2m+1)
+  float2* st_ga2 = reinterpret_cast<float2*>(sbase + (H2C ? 0 : 2 * E * T)) + t;
   float acc_d[E], acc_b[E];
 #pragma unroll
   for (int i = 0; i < E; ++i) {
     acc_d[i] = acc_b[i] = 0.f;
-    st_ga[i * T] = 0.f;
+    if constexpr (G::FP) {
+      if (i < E / 2) st_ga2[i * T] = make_float2(0.f, 0.f);
+    } else {
+      st_ga[i * T] = 0.f;
+    }
   }
   const int64_t npairs = (p.rows + 1) >> 1;
 
@@ -342,8 +348,7 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
           acc_d[2 * s] = fmaf(hl.x, g3l.x, fmaf(hl.y, g3l.y, acc_d[2 * s]));
           acc_d[2 * s + 1] = fmaf(hh.x, g3h.x, fmaf(hh.y, g3h.y, acc_d[2 * s + 1]));
           const float dl = ld_plain(fm.plo(p.d, s)), dh = ld_plain(fm.phi(p.d, s));
-          dct3_pre(make_float2(g3l.x * dl, g3l.y * dl), make_float2(g3h.x * dh, g3h.y * dh), cs, fm.special(s), chi,
-                   gl[s], gh[s]);
+          dct3_pre(vmul(bc(dl), g3l), vmul(bc(dh), g3h), cs, fm.special(s), chi, gl[s], gh[s]);
         }
         fp_scatter<G>(gl, gh, v, fm);
       } else {
@@ -375,8 +380,7 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
           acc_d[2 * s] = fmaf(hl.x, g3l.x, fmaf(hl.y, g3l.y, acc_d[2 * s]));
           acc_d[2 * s + 1] = fmaf(hh.x, g3h.x, fmaf(hh.y, g3h.y, acc_d[2 * s + 1]));
           const float dl = ld_plain(fm.plo(p.d, s)), dh = ld_plain(fm.phi(p.d, s));
-          dct3_pre(make_float2(g3l.x * dl, g3l.y * dl), make_float2(g3h.x * dh, g3h.y * dh), cs, fm.special(s), chi,
-                   gl[s], gh[s]);
+          dct3_pre(vmul(bc(dl), g3l), vmul(bc(dh), g3h), cs, fm.special(s), chi, gl[s], gh[s]);
         }
         fp_scatter<G>(gl, gh, v, fm);
       }
@@ -405,10 +409,9 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
       for (int q = 0; q < 8; ++q) {
         const float2 av = ld_f2(pa + 2 * q * S);
         if (!hasb) xbv[q] = make_float2(0.f, 0.f);
-        st_ga[(2 * q) * T] += fmaf(gb[q].x, xbv[q].x, ga[q].x * xav[q].x);
-        st_ga[(2 * q + 1) * T] += fmaf(gb[q].y, xbv[q].y, ga[q].y * xav[q].y);
-        float2 da = make_float2(av.x * ga[q].x, av.y * ga[q].y);
-        float2 db = make_float2(av.x * gb[q].x, av.y * gb[q].y);
+        st_ga2[q * T] = cadd(st_ga2[q * T], vfma(gb[q], xbv[q], vmul(ga[q], xav[q])));
+        float2 da = vmul(av, ga[q]);
+        float2 db = vmul(av, gb[q]);
         if (relu) {  // previous block's ReLU: mask = x > 0 (layers.py:227, 233)
           da = make_float2(xav[q].x > 0.f ? da.x : 0.f, xav[q].y > 0.f ? da.y : 0.f);
           db = make_float2(xbv[q].x > 0.f ? db.x : 0.f, xbv[q].y > 0.f ? db.y : 0.f);
@@ -442,8 +445,9 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
     float* w = p.ws + c.gid * 3 * G::N;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      w[2 * (fm.jsp + q * S)] = st_ga[(2 * q) * T];
-      w[2 * (fm.jsp + q * S) + 1] = st_ga[(2 * q + 1) * T];
+      const float2 g = st_ga2[q * T];
+      w[2 * (fm.jsp + q * S)] = g.x;
+      w[2 * (fm.jsp + q * S) + 1] = g.y;
     }
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
@@ -500,8 +504,8 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
         acc_d[2 * i] = fmaf(hl.x, gl.x, fmaf(hl.y, gl.y, acc_d[2 * i]));
         acc_d[2 * i + 1] = fmaf(hh.x, gh.x, fmaf(hh.y, gh.y, acc_d[2 * i + 1]));
         const float dl = ld_plain(sl.plo(p.d, i)), dh = ld_plain(sl.phi(p.d, i));
-        Y[2 * i] = make_float2(gl.x * dl, gl.y * dl);
-        Y[2 * i + 1] = make_float2(gh.x * dh, gh.y * dh);
+        Y[2 * i] = vmul(bc(dl), gl);
+        Y[2 * i + 1] = vmul(bc(dh), gh);
       }
     }
     // g1 = C3(Y); dx = a * g1; grad_a partial += x * g1

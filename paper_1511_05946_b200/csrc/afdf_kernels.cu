@@ -45,7 +45,7 @@ __device__ __forceinline__ float2 ld_param(const float2* p) {
 
 __device__ __forceinline__ float2 conjf2(float2 z) { return make_float2(z.x, -z.y); }
 __device__ __forceinline__ float2 cmul_conj(float2 a, float2 b) {  // a * conj(b)
-  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
+  return vfma(bc(b.y), mul_ni(a), vmul(bc(b.x), a));
 }
 
 template <class G>

@@ -80,8 +80,8 @@ __global__ void ACDC_LB(Geo<LOGN>) cascade_fwd_kernel(CParams p) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const float2 s2 = ld_plain_f2(pav + 2 * q * S);
-          pa[q] = make_float2(pa[q].x * s2.x, pa[q].y * s2.y);
-          pb[q] = make_float2(pb[q].x * s2.x, pb[q].y * s2.y);
+          pa[q] = vmul(pa[q], s2);
+          pb[q] = vmul(pb[q], s2);
         }
         fp_from_pairs<G>(v, pa, pb, fm);
       }
@@ -98,8 +98,8 @@ __global__ void ACDC_LB(Geo<LOGN>) cascade_fwd_kernel(CParams p) {
           __stcs(hc + s * T, make_float4(xl.x, xl.y, xh.x, xh.y));
           const float dlo = ld_plain(fm.plo(dl, s)), blo = ld_plain(fm.plo(bl, s));
           const float dhi = ld_plain(fm.phi(dl, s)), bhi = ld_plain(fm.phi(bl, s));
-          xl = make_float2(fmaf(xl.x, dlo, blo), fmaf(xl.y, dlo, blo));
-          xh = make_float2(fmaf(xh.x, dhi, bhi), fmaf(xh.y, dhi, bhi));
+          xl = vfma(xl, bc(dlo), bc(blo));
+          xh = vfma(xh, bc(dhi), bc(bhi));
           dct3_pre(xl, xh, cs, fm.special(s), chi, gl[s], gh[s]);
         }
         fp_scatter<G>(gl, gh, v, fm);

@@ -86,36 +86,34 @@ __device__ __forceinline__ void gather_pairs(const float2 (&v)[G::E], float2 (&z
 }
 
 // DCT-II post-pass for one slot: (Z[lo], Z[hi]) -> X[lo] = (XA, XB), X[hi].
+// With U = Z[lo] + Z[hi] and M = Z[lo] - Z[hi] the four outputs are
+//   X[lo] = c.x U + c.y (i M),   X[hi] = c.x (i M) - c.y U
+// (expanding XA = Re c(P+Q), XB = Re c(-i)(P-Q) etc.): 6 packed instructions.
 __device__ __forceinline__ void dct2_post(float2 zlo, float2 zhi, float2 c, bool special, float2 c_hi, float2& xlo,
                                           float2& xhi) {
   if (special) {
-    const float f0 = 2.f * c.x, fh = 2.f * c_hi.x;
-    xlo = make_float2(f0 * zlo.x, f0 * zlo.y);
-    xhi = make_float2(fh * zhi.x, fh * zhi.y);
+    xlo = vmul(bc(2.f * c.x), zlo);
+    xhi = vmul(bc(2.f * c_hi.x), zhi);
   } else {
-    const float2 q = make_float2(zhi.x, -zhi.y);
-    const float2 s = cadd(zlo, q);
-    const float2 dn = mul_ni(csub(zlo, q));
-    const float2 wa = cmul(s, c);
-    const float2 wb = cmul(dn, c);
-    xlo = make_float2(wa.x, wb.x);
-    xhi = make_float2(-wa.y, -wb.y);
+    const float2 u = cadd(zlo, zhi), m = csub(zlo, zhi);
+    const float2 im = make_float2(-m.y, m.x);
+    xlo = vfma(bc(c.y), im, vmul(bc(c.x), u));
+    xhi = vfma(bc(c.x), im, vmul(bc(-c.y), u));
   }
 }
 
 // DCT-III pre-pass for one slot: Y[lo] = (YA, YB), Y[hi] -> G[lo], G[hi].
+// With K = Y[lo] - i Y[hi] and L = Y[lo] + i Y[hi] (u = conj c):
+//   G[lo] = c.x conj(K) + c.y swap(K),   G[hi] = c.x conj(L) - c.y swap(L).
 __device__ __forceinline__ void dct3_pre(float2 ylo, float2 yhi, float2 c, bool special, float2 c_hi, float2& glo,
                                          float2& ghi) {
   if (special) {
-    const float f0 = 2.f * c.x, fh = 2.f * c_hi.x;
-    glo = make_float2(f0 * ylo.x, -f0 * ylo.y);
-    ghi = make_float2(fh * yhi.x, -fh * yhi.y);
+    glo = vmul(bc(2.f * c.x), make_float2(ylo.x, -ylo.y));
+    ghi = vmul(bc(2.f * c_hi.x), make_float2(yhi.x, -yhi.y));
   } else {
-    const float2 u = make_float2(c.x, -c.y);
-    const float2 ua = cmul(make_float2(ylo.x, -yhi.x), u);
-    const float2 ub = cmul(make_float2(ylo.y, -yhi.y), u);
-    glo = make_float2(ua.x - ub.y, -ua.y - ub.x);
-    ghi = make_float2(ua.x + ub.y, ua.y - ub.x);
+    const float2 k = cadd_ni(ylo, yhi), l = cadd_pi(ylo, yhi);
+    glo = vfma(bc(c.y), make_float2(k.y, k.x), vmul(bc(c.x), make_float2(k.x, -k.y)));
+    ghi = vfma(bc(-c.y), make_float2(l.y, l.x), vmul(bc(c.x), make_float2(l.x, -l.y)));
   }
 }
 
@@ -224,8 +222,8 @@ __device__ __forceinline__ void fp_load(float2 (&v)[16], const float* xa, const 
     float2 b2 = xb ? ld_f2(pb + 2 * q * S) : make_float2(0.f, 0.f);
     if constexpr (SCALE) {
       const float2 s2 = ld_f2(ps + 2 * q * S);
-      a2 = make_float2(a2.x * s2.x, a2.y * s2.y);
-      b2 = make_float2(b2.x * s2.x, b2.y * s2.y);
+      a2 = vmul(a2, s2);
+      b2 = vmul(b2, s2);
     }
     v[q] = make_float2(a2.x, b2.x);
     snd[q] = make_float2(a2.y, b2.y);

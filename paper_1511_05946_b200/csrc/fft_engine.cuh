@@ -33,14 +33,43 @@
 namespace acdc {
 
 // ------------------------------------------------------------ complex helpers
+// sm_100 executes fp32 pairs as ONE instruction (FADD2 / FMUL2 / FFMA2, PTX
+// add/mul/fma.rn.f32x2), and the packed operands take a lane swap (.LO_HI),
+// a hi-lane negation (.NP), a whole-operand negation and a scalar broadcast
+// (.F32 / immediate) for free.  A complex value is one register pair, so
+// every complex add is one FADD2, z * (-i) folds into the consumer's operand
+// and a complex multiply is FMUL2 + FFMA2 (scalar: 4 FP instructions).  The
+// probe (scripts/fp32x2_probe.cu) measures the same lane throughput for
+// FFMA2 and FFMA, so the gain is issue slots: the FP instructions of the FFT
+// halve.  -DACDC_SCALAR_FP builds the scalar forms for A/B comparisons.
+#ifndef ACDC_SCALAR_FP
+#define ACDC_PACKED 1
+#endif
+__device__ __forceinline__ float2 bc(float s) { return make_float2(s, s); }
+#ifdef ACDC_PACKED
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+// a + (-i) b  and  a + i b
+__device__ __forceinline__ float2 cadd_ni(float2 a, float2 b) { return __fadd2_rn(a, make_float2(b.y, -b.x)); }
+__device__ __forceinline__ float2 cadd_pi(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.y, b.x)); }
+// lane-wise a * b, a * b + c
+__device__ __forceinline__ float2 vmul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 vfma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+#else
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cadd_ni(float2 a, float2 b) { return make_float2(a.x + b.y, a.y - b.x); }
+__device__ __forceinline__ float2 cadd_pi(float2 a, float2 b) { return make_float2(a.x - b.y, a.y + b.x); }
+__device__ __forceinline__ float2 vmul(float2 a, float2 b) { return make_float2(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ float2 vfma(float2 a, float2 b, float2 c) {
+  return make_float2(fmaf(a.x, b.x, c.x), fmaf(a.y, b.y, c.y));
+}
+#endif
+// a * w = w.x a + w.y (i a)
 __device__ __forceinline__ float2 cmul(float2 a, float2 w) {
-  return make_float2(fmaf(a.x, w.x, -a.y * w.y), fmaf(a.x, w.y, a.y * w.x));
+  return vfma(make_float2(-a.y, a.x), bc(w.y), vmul(bc(w.x), a));
 }
-__device__ __forceinline__ float2 cmulc(float2 z, float wr, float wi) {
-  return make_float2(fmaf(z.x, wr, -z.y * wi), fmaf(z.x, wi, z.y * wr));
-}
+__device__ __forceinline__ float2 cmulc(float2 z, float wr, float wi) { return cmul(z, make_float2(wr, wi)); }
 // -i * z
 __device__ __forceinline__ float2 mul_ni(float2 z) { return make_float2(z.y, -z.x); }
 
@@ -58,6 +87,7 @@ __device__ __forceinline__ float2 ldg_f2_volatile(const float2* p) {
 
 // ------------------------------------------------------------ DFT butterflies
 // All take a[0..R) in natural order and return the forward DFT in natural order.
+// Written so every step is one packed instruction (see the helpers above).
 __device__ __forceinline__ void dft2(float2& a0, float2& a1) {
   float2 t = a0;
   a0 = cadd(t, a1);
@@ -69,26 +99,26 @@ __device__ __forceinline__ void dft4(float2& a0, float2& a1, float2& a2, float2&
   float2 t2 = cadd(a1, a3), t3 = csub(a1, a3);
   a0 = cadd(t0, t2);
   a2 = csub(t0, t2);
-  a1 = cadd(t1, mul_ni(t3));
-  a3 = csub(t1, mul_ni(t3));
+  a1 = cadd_ni(t1, t3);
+  a3 = cadd_pi(t1, t3);
 }
 
-// z * W8^1 = z * (h, -h);  z * W8^3 = z * (-h, -h)
-__device__ __forceinline__ float2 mul_w8_1(float2 z) { return make_float2(ACDC_H * (z.x + z.y), ACDC_H * (z.y - z.x)); }
-__device__ __forceinline__ float2 mul_w8_3(float2 z) { return make_float2(ACDC_H * (z.y - z.x), -ACDC_H * (z.x + z.y)); }
+// z * W8^1 = H (x + y, y - x);  z * W8^3 = -H (x - y, x + y)
+__device__ __forceinline__ float2 mul_w8_1(float2 z) { return vmul(bc(ACDC_H), cadd_ni(z, z)); }
+__device__ __forceinline__ float2 mul_w8_3(float2 z) { return vmul(bc(-ACDC_H), cadd_pi(z, z)); }
 
 __device__ __forceinline__ void dft8(float2* a) {
   // decimation in time: E = DFT4(even), O = DFT4(odd)
   dft4(a[0], a[2], a[4], a[6]);
   dft4(a[1], a[3], a[5], a[7]);
-  float2 o1 = mul_w8_1(a[3]), o2 = mul_ni(a[5]), o3 = mul_w8_3(a[7]);
-  float2 e0 = a[0], e1 = a[2], e2 = a[4], e3 = a[6];
+  float2 o1 = mul_w8_1(a[3]), o3 = mul_w8_3(a[7]);
+  float2 e0 = a[0], e1 = a[2], e2 = a[4], e3 = a[6], o2 = a[5];
   a[0] = cadd(e0, a[1]);
   a[4] = csub(e0, a[1]);
   a[1] = cadd(e1, o1);
   a[5] = csub(e1, o1);
-  a[2] = cadd(e2, o2);
-  a[6] = csub(e2, o2);
+  a[2] = cadd_ni(e2, o2);
+  a[6] = cadd_pi(e2, o2);
   a[3] = cadd(e3, o3);
   a[7] = csub(e3, o3);
 }
@@ -103,17 +133,17 @@ __device__ __forceinline__ void dft8(float2* a) {
 //   out0 = t0 + t2, out2 = t0 - t2, out1 = t1 - i t3, out3 = t1 + i t3.
 __device__ __forceinline__ void dft4_tail(float2 t0, float2 t1, float2 e, float2 f, float c, float2& o0, float2& o1,
                                           float2& o2, float2& o3) {
-  o0 = make_float2(fmaf(c, e.x, t0.x), fmaf(c, e.y, t0.y));
-  o2 = make_float2(fmaf(-c, e.x, t0.x), fmaf(-c, e.y, t0.y));
-  o1 = make_float2(fmaf(c, f.y, t1.x), fmaf(-c, f.x, t1.y));
-  o3 = make_float2(fmaf(-c, f.y, t1.x), fmaf(c, f.x, t1.y));
+  o0 = vfma(bc(c), e, t0);
+  o2 = vfma(bc(-c), e, t0);
+  o1 = vfma(bc(c), mul_ni(f), t1);
+  o3 = vfma(bc(-c), mul_ni(f), t1);
 }
 // z W^1 = C1 (x + T1 y, y - T1 x);  z W^3 = C1 (T1 x + y, T1 y - x);  z W^9 = -(z W^1 form)
-__device__ __forceinline__ float2 tw1_r(float2 z) { return make_float2(fmaf(ACDC_T1, z.y, z.x), fmaf(-ACDC_T1, z.x, z.y)); }
-__device__ __forceinline__ float2 tw3_s(float2 z) { return make_float2(fmaf(ACDC_T1, z.x, z.y), fmaf(ACDC_T1, z.y, -z.x)); }
-// z W^2 = H (x + y, y - x);  z W^6 = H (y - x, -(x + y))
-__device__ __forceinline__ float2 tw2_p(float2 z) { return make_float2(z.x + z.y, z.y - z.x); }
-__device__ __forceinline__ float2 tw6_q(float2 z) { return make_float2(z.y - z.x, -(z.x + z.y)); }
+__device__ __forceinline__ float2 tw1_r(float2 z) { return vfma(bc(ACDC_T1), mul_ni(z), z); }
+__device__ __forceinline__ float2 tw3_s(float2 z) { return vfma(bc(ACDC_T1), z, mul_ni(z)); }
+// z W^2 = H (x + y, y - x);  z W^6 = H (y - x, -(x + y)) = -H (x - y, x + y)
+__device__ __forceinline__ float2 tw2_p(float2 z) { return cadd_ni(z, z); }
+__device__ __forceinline__ float2 tw6_qn(float2 z) { return cadd_pi(z, z); }  // = -(z W^6) / H
 
 __device__ __forceinline__ void dft16(float2* a) {
   // 4 x 4: n = 4 n1 + n2, k = k1 + 4 k2
@@ -121,26 +151,26 @@ __device__ __forceinline__ void dft16(float2* a) {
   for (int n2 = 0; n2 < 4; ++n2) dft4(a[n2], a[n2 + 4], a[n2 + 8], a[n2 + 12]);
 #ifdef ACDC_DFT16_FMA
   // a[n2 + 4 k1] * W16^(n2 k1), then DFT4 over n2, with every non-trivial
-  // twiddle folded into FMAs (80 instead of 96 instructions for this stage).
+  // twiddle folded into FMAs.
   float2 o[16];
   dft4(a[0], a[1], a[2], a[3]);
   o[0] = a[0], o[4] = a[1], o[8] = a[2], o[12] = a[3];
   {  // k1 = 1: W^1, W^2, W^3 (common factor C1 for the odd pair)
     const float2 p = tw2_p(a[6]), r = tw1_r(a[5]), s = tw3_s(a[7]);
-    const float2 t0 = make_float2(fmaf(ACDC_H, p.x, a[4].x), fmaf(ACDC_H, p.y, a[4].y));
-    const float2 t1 = make_float2(fmaf(-ACDC_H, p.x, a[4].x), fmaf(-ACDC_H, p.y, a[4].y));
+    const float2 t0 = vfma(bc(ACDC_H), p, a[4]);
+    const float2 t1 = vfma(bc(-ACDC_H), p, a[4]);
     dft4_tail(t0, t1, cadd(r, s), csub(r, s), ACDC_C1, o[1], o[5], o[9], o[13]);
   }
   {  // k1 = 2: W^2, W^4 = -i, W^6 (common factor H)
-    const float2 p = tw2_p(a[9]), q = tw6_q(a[11]);
-    const float2 t0 = make_float2(a[8].x + a[10].y, a[8].y - a[10].x);
-    const float2 t1 = make_float2(a[8].x - a[10].y, a[8].y + a[10].x);
-    dft4_tail(t0, t1, cadd(p, q), csub(p, q), ACDC_H, o[2], o[6], o[10], o[14]);
+    const float2 p = tw2_p(a[9]), qn = tw6_qn(a[11]);
+    const float2 t0 = cadd_ni(a[8], a[10]);
+    const float2 t1 = cadd_pi(a[8], a[10]);
+    dft4_tail(t0, t1, csub(p, qn), cadd(p, qn), ACDC_H, o[2], o[6], o[10], o[14]);
   }
   {  // k1 = 3: W^3, W^6, W^9 = -(W^1 form)
-    const float2 q = tw6_q(a[14]), s = tw3_s(a[13]), r = tw1_r(a[15]);
-    const float2 t0 = make_float2(fmaf(ACDC_H, q.x, a[12].x), fmaf(ACDC_H, q.y, a[12].y));
-    const float2 t1 = make_float2(fmaf(-ACDC_H, q.x, a[12].x), fmaf(-ACDC_H, q.y, a[12].y));
+    const float2 qn = tw6_qn(a[14]), s = tw3_s(a[13]), r = tw1_r(a[15]);
+    const float2 t0 = vfma(bc(-ACDC_H), qn, a[12]);
+    const float2 t1 = vfma(bc(ACDC_H), qn, a[12]);
     dft4_tail(t0, t1, csub(s, r), cadd(s, r), ACDC_C1, o[3], o[7], o[11], o[15]);
   }
 #pragma unroll
@@ -184,6 +214,16 @@ __device__ __forceinline__ void dft(float2* a) {
 }
 
 // ------------------------------------------------------------ geometry
+// Radix-16 pass twiddles from 4 loaded powers (W^k, W^2k, W^4k, W^8k) and 11
+// packed complex products (2 instructions each) instead of 15 loads: the
+// twiddle shared-memory traffic drops 4x (the forward is bound by the
+// shared-memory pipe) and the table shrinks from 18 to 4 float2 per k.  The
+// products add <= 3 roundings (|err| < 4e-7, far inside the parity bound).
+#ifndef ACDC_NO_TWGEN
+#define ACDC_TWGEN 1
+#else
+#define ACDC_TWGEN 0
+#endif
 // Radix plan and per-pass twiddle-table layout for N = 2^LOGN (16 x small x 16...).
 template <int LOGN>
 struct Plan {
@@ -200,7 +240,9 @@ struct Plan {
   // pass p >= 1 twiddles W_{Ns R}^{q k}, stored at tw_off(p) + k*tw_stride(R) + (q-1):
   // one row per butterfly k so consecutive q pairs load as one 128-bit LDS; the
   // row stride (R+2 float2, or 1 for R = 2) keeps 8 consecutive k on disjoint banks.
-  __host__ __device__ static constexpr int tw_stride(int r) { return r == 2 ? 1 : r + 2; }
+  // Radix-16 passes (ACDC_TWGEN) store only W^k, W^2k (float4 at tw_off + 2k) and
+  // W^4k, W^8k (float4 at tw_off + 2 Ns + 2k); the other 11 are products.
+  __host__ __device__ static constexpr int tw_stride(int r) { return r == 2 ? 1 : ((r == 16 && ACDC_TWGEN) ? 4 : r + 2); }
   __host__ __device__ static constexpr int tw_off(int p) {
     return p <= 1 ? 0 : tw_off(p - 1) + tw_stride(radix(p - 1)) * span(p - 1);
   }
@@ -384,7 +426,29 @@ __device__ __forceinline__ void pass_compute(float2 (&v)[G::E], const float2* tw
     if constexpr (NS > 1) {
       const int k = (j0 + b * G::T) & (NS - 1);
       const float2* row = tw + G::tw_off(P) + k * G::tw_stride(R);  // row[q-1] = W_{NS R}^{q k}
-      if constexpr (R == 2) {
+      if constexpr (R == 16 && ACDC_TWGEN) {
+        const float4 w12 = tab_load4<G>(tw + G::tw_off(P) + 2 * k);
+        const float4 w48 = tab_load4<G>(tw + G::tw_off(P) + 2 * NS + 2 * k);
+        float2* a = &v[b * R];
+        const float2 w1 = make_float2(w12.x, w12.y), w2 = make_float2(w12.z, w12.w);
+        const float2 w4 = make_float2(w48.x, w48.y), w8 = make_float2(w48.z, w48.w);
+        const float2 w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
+        a[1] = cmul(a[1], w1);
+        a[2] = cmul(a[2], w2);
+        a[3] = cmul(a[3], w3);
+        a[4] = cmul(a[4], w4);
+        a[5] = cmul(a[5], w5);
+        a[6] = cmul(a[6], w6);
+        a[7] = cmul(a[7], w7);
+        a[8] = cmul(a[8], w8);
+        a[9] = cmul(a[9], cmul(w1, w8));
+        a[10] = cmul(a[10], cmul(w2, w8));
+        a[11] = cmul(a[11], cmul(w3, w8));
+        a[12] = cmul(a[12], cmul(w4, w8));
+        a[13] = cmul(a[13], cmul(w5, w8));
+        a[14] = cmul(a[14], cmul(w6, w8));
+        a[15] = cmul(a[15], cmul(w7, w8));
+      } else if constexpr (R == 2) {
         v[b * R + 1] = cmul(v[b * R + 1], tab_load<G>(row, 0));
       } else {
 #pragma unroll

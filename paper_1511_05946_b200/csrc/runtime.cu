@@ -54,6 +54,13 @@ static float2 twiddle(long m, long M) {
   return make_float2((float)std::cos(th), (float)-std::sin(th));
 }
 
+// fft_engine.cuh ACDC_TWGEN: radix-16 passes keep only W^k, W^2k, W^4k, W^8k.
+#ifndef ACDC_NO_TWGEN
+#define ACDC_TWGEN_HOST 1
+#else
+#define ACDC_TWGEN_HOST 0
+#endif
+
 // Host mirror of Plan<LOGN> (radix 16 x small x 16 ...), fft_engine.cuh.
 static void host_plan(int logn, std::vector<int>& radix) {
   radix.clear();
@@ -86,6 +93,13 @@ int get_tables(int logn, Tables* out) {
   long ns = radix[0];
   for (size_t p = 1; p < radix.size(); ++p) {
     const int r = radix[p];
+    if (r == 16 && ACDC_TWGEN_HOST) {  // [k](W^k, W^2k) then [k](W^4k, W^8k)
+      for (int half = 0; half < 2; ++half)
+        for (long k = 0; k < ns; ++k)
+          for (int e = 0; e < 2; ++e) h.push_back(twiddle((long)(1 << (2 * half + e)) * k, ns * r));
+      ns *= r;
+      continue;
+    }
     const int stride = r == 2 ? 1 : r + 2;
     for (long k = 0; k < ns; ++k)
       for (int slot = 0; slot < stride; ++slot)
