@@ -132,6 +132,9 @@ __device__ __forceinline__ void packed_dct3(float2 (&Y)[G::E], float2 (&v)[G::E]
 #ifndef ACDC_BWD_CTA
 #define ACDC_BWD_CTA 0
 #endif
+#ifndef ACDC_PF_DIST  // L2 prefetch distance in row-pair iterations (fast-pairing kernels)
+#define ACDC_PF_DIST 1
+#endif
 template <int LOGN, int CTA>
 constexpr int fp_gpc() {
   return (CTA && Geo<LOGN>::FP && Geo<LOGN>::T <= CTA / 2) ? CTA / Geo<LOGN>::T : 0;
@@ -178,8 +181,8 @@ __global__ void ACDC_LB(GeoFwd<LOGN>) acdc_fwd_kernel(KParams p) {
     for (int64_t rp = c.gid; rp < npairs; rp += c.gstride) {
       const int64_t ra = 2 * rp;
       const bool hasb = ra + 1 < p.rows;
-      if (t == 0 && rp + c.gstride < npairs) {  // next row pair -> L2
-        const int64_t nr = 2 * (rp + c.gstride);
+      if (t == 0 && rp + ACDC_PF_DIST * c.gstride < npairs) {  // a later row pair -> L2
+        const int64_t nr = 2 * (rp + ACDC_PF_DIST * c.gstride);
         prefetch_row_l2(p.x + nr * p.ldx, G::N);
         if (nr + 1 < p.rows) prefetch_row_l2(p.x + (nr + 1) * p.ldx, G::N);
       }
@@ -220,8 +223,8 @@ __global__ void ACDC_LB(GeoFwd<LOGN>) acdc_fwd_kernel(KParams p) {
       float2* yb = reinterpret_cast<float2*>(p.y + (hasb ? ra + 1 : ra) * p.ldo + 2 * fm.jsp);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        ya[q * FastMap<G>::S] = oa[q];
-        if (hasb) yb[q * FastMap<G>::S] = ob[q];
+        st_row_f2(ya + q * FastMap<G>::S, oa[q]);
+        if (hasb) st_row_f2(yb + q * FastMap<G>::S, ob[q]);
       }
     }
     return;
@@ -273,6 +276,17 @@ __global__ void ACDC_LB(GeoFwd<LOGN>) acdc_fwd_kernel(KParams p) {
 template <int LOGN, bool H2C = false>
 using GeoBwd = Geo<LOGN, (H2C ? 1 : 3) * Geo<LOGN>::E, (H2C ? fp_gpc<LOGN, ACDC_BWD_CTA>() : 0)>;
 
+// Backward parameter stash (fast-pairing path): d at every thread's 8 spectral
+// slots, [slot][t] float2 (d_lo, d_hi), shared by the CTA's groups and filled
+// once per launch.  The slot pass then has no global parameter loads, so the
+// h2-cache loads can all be issued at its top (one exposed latency per row
+// pair instead of one per slot).
+template <int LOGN, bool H2C>
+__host__ __device__ constexpr int bwd_dstash_bytes() {
+  using G = GeoBwd<LOGN, H2C>;
+  return (G::FP && G::TW_SMEM && G::SMEM_BYTES + 8 * G::T * 8 <= G::SMEM_LIMIT) ? 8 * G::T * 8 : 0;
+}
+
 // H2C: read h2 from the forward's cache instead of recomputing C2(a * x);
 // the backward then runs 2 packed FFTs instead of 3 and needs no g3 stash.
 template <int LOGN, bool H2C>
@@ -291,6 +305,17 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
   float* sbase = G::STASH_SMEM ? gbase + G::NBUF * G::BUF_FLOATS : p.scratch + c.gid * G::GSCRATCH_FLOATS;
   float2* st_g3 = reinterpret_cast<float2*>(sbase) + t;  // [E][T]
   float* st_ga = sbase + (H2C ? 0 : 2 * E * T) + t;     // [E][T]
+  constexpr bool DST = bwd_dstash_bytes<LOGN, H2C>() > 0;
+  const float2* dst = reinterpret_cast<const float2*>(smem_f + G::SMEM_BYTES / 4) + t;
+  if constexpr (DST) {  // group 0 fills; stage_tables' barrier publishes it
+    const FastMap<G> fm(t, gs.mask);
+    if (c.grp == 0) {
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        reinterpret_cast<float2*>(smem_f + G::SMEM_BYTES / 4)[t + s * T] =
+            make_float2(__ldg(fm.plo(p.d, s)), __ldg(fm.phi(p.d, s)));
+    }
+  }
   const float2 *tw, *cp;
   stage_tables<G>(p.tab, smem_f, tw, cp);
   // fast-pairing path: grad_a partials as float2 [q][T] (positions 2m, 2m+1)
@@ -317,14 +342,17 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
       const bool hasb = ra + 1 < p.rows;
       const float* xa = p.x + ra * p.ldx;
       const float* xbp = hasb ? p.x + (ra + 1) * p.ldx : nullptr;
-      if (t == 0 && rp + c.gstride < npairs) {  // next row pair -> L2
-        const int64_t nr = 2 * (rp + c.gstride);
+      if (t == 0 && rp + ACDC_PF_DIST * c.gstride < npairs) {  // a later row pair -> L2
+        const int64_t nrp = rp + ACDC_PF_DIST * c.gstride, nr = 2 * nrp;
         prefetch_row_l2(p.dy + nr * p.ldy, G::N);
         prefetch_row_l2(p.x + nr * p.ldx, G::N);
         if (nr + 1 < p.rows) {
           prefetch_row_l2(p.dy + (nr + 1) * p.ldy, G::N);
           prefetch_row_l2(p.x + (nr + 1) * p.ldx, G::N);
         }
+#ifdef ACDC_PF_H2
+        if constexpr (H2C) prefetch_row_l2(p.h2c + nrp * 2 * G::N, 2 * G::N);
+#endif
       }
       float2 v[16];
       const float2 chi = tab_load<G>(cp, G::N / 2);
@@ -334,8 +362,11 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
       if constexpr (H2C) {
         // g3 and the cached h2 in one slot pass: grad_bias, grad_d, Y = d * g3
         float2 w[8], gl[8], gh[8];
-        fp_partner<G>(v, w, fm);
         const float4* hc = reinterpret_cast<const float4*>(p.h2c + rp * 2 * G::N) + t;
+        float4 h2v[8];
+#pragma unroll
+        for (int s = 0; s < 8; ++s) h2v[s] = __ldcs(hc + s * G::T);  // all in flight before any use
+        fp_partner<G>(v, w, fm);
 #pragma unroll
         for (int s = 0; s < 8; ++s) {
           const float2 cs = tab_load<G>(fm.plo(cp, s), 0);
@@ -343,11 +374,17 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
           dct2_post(v[s], w[s], cs, fm.special(s), chi, g3l, g3h);
           acc_b[2 * s] += g3l.x + g3l.y;
           acc_b[2 * s + 1] += g3h.x + g3h.y;
-          const float4 h4 = __ldcs(hc + s * G::T);
+          const float4 h4 = h2v[s];
           const float2 hl = make_float2(h4.x, h4.y), hh = make_float2(h4.z, h4.w);
           acc_d[2 * s] = fmaf(hl.x, g3l.x, fmaf(hl.y, g3l.y, acc_d[2 * s]));
           acc_d[2 * s + 1] = fmaf(hh.x, g3h.x, fmaf(hh.y, g3h.y, acc_d[2 * s + 1]));
-          const float dl = ld_plain(fm.plo(p.d, s)), dh = ld_plain(fm.phi(p.d, s));
+          float dl, dh;
+          if constexpr (DST) {
+            const float2 dv = dst[s * T];
+            dl = dv.x, dh = dv.y;
+          } else {
+            dl = ld_plain(fm.plo(p.d, s)), dh = ld_plain(fm.phi(p.d, s));
+          }
           dct3_pre(vmul(bc(dl), g3l), vmul(bc(dh), g3h), cs, fm.special(s), chi, gl[s], gh[s]);
         }
         fp_scatter<G>(gl, gh, v, fm);
@@ -379,17 +416,35 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
           const float2 g3l = st_g3[(2 * s) * T], g3h = st_g3[(2 * s + 1) * T];
           acc_d[2 * s] = fmaf(hl.x, g3l.x, fmaf(hl.y, g3l.y, acc_d[2 * s]));
           acc_d[2 * s + 1] = fmaf(hh.x, g3h.x, fmaf(hh.y, g3h.y, acc_d[2 * s + 1]));
-          const float dl = ld_plain(fm.plo(p.d, s)), dh = ld_plain(fm.phi(p.d, s));
+          float dl, dh;
+          if constexpr (DST) {
+            const float2 dv = dst[s * T];
+            dl = dv.x, dh = dv.y;
+          } else {
+            dl = ld_plain(fm.plo(p.d, s)), dh = ld_plain(fm.phi(p.d, s));
+          }
           dct3_pre(vmul(bc(dl), g3l), vmul(bc(dh), g3h), cs, fm.special(s), chi, gl[s], gh[s]);
         }
         fp_scatter<G>(gl, gh, v, fm);
       }
       }  // !H2C
       // g1 = C3(d * g3); dx = a * g1; grad_a partial += x * g1
+      const int64_t rb = hasb ? ra + 1 : ra;
+#ifdef ACDC_BWD_XPRE  // experiment: x loads in flight across the last FFT
+      float2 xav[8], xbv[8];
+      {
+        const float* pxa = xa + 2 * fm.jsp;
+        const float* pxb = p.x + rb * p.ldx + 2 * fm.jsp;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          xav[q] = ld_row_f2(pxa + 2 * q * S);
+          xbv[q] = ld_row_f2(pxb + 2 * q * S);
+        }
+      }
+#endif
       fft_passes<G, 0>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
       float2 ga[8], gb[8];
       fp_out_pairs<G>(v, ga, gb, fm);
-      const int64_t rb = hasb ? ra + 1 : ra;
       float2* oa = reinterpret_cast<float2*>(p.y + ra * p.ldo + 2 * fm.jsp);
       float2* ob = reinterpret_cast<float2*>(p.y + rb * p.ldo + 2 * fm.jsp);
       const float* pxa = xa + 2 * fm.jsp;
@@ -398,12 +453,14 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
       // All x / a loads of the row pair are issued before any store or
       // volatile index load, so their L2 latencies overlap instead of
       // serialising once per q.
+#ifndef ACDC_BWD_XPRE
       float2 xav[8], xbv[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        xav[q] = ld_f2(pxa + 2 * q * S);
-        xbv[q] = ld_f2(pxb + 2 * q * S);  // row rb == ra when !hasb: in bounds, unused
+        xav[q] = ld_row_f2(pxa + 2 * q * S);
+        xbv[q] = ld_row_f2(pxb + 2 * q * S);  // row rb == ra when !hasb: in bounds, unused
       }
+#endif
       const bool relu = p.epi_relu;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -436,8 +493,8 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
       } else {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          oa[q * S] = ga[q];
-          if (hasb) ob[q * S] = gb[q];
+          st_row_f2(oa + q * S, ga[q]);
+          if (hasb) st_row_f2(ob + q * S, gb[q]);
         }
       }
     }
@@ -714,6 +771,7 @@ static LaunchInfo info_for(int kind) {
     case K_BWD:
       li.fn = (const void*)acdc_bwd_kernel<LOGN, false>;
       geom<GB>(li, GB::GSCRATCH_FLOATS);
+      li.smem += bwd_dstash_bytes<LOGN, false>();
       break;
     case K_DCT2:
       li.fn = (const void*)acdc_dct2_kernel<LOGN>;
@@ -731,6 +789,7 @@ static LaunchInfo info_for(int kind) {
     default:
       li.fn = FP ? (const void*)acdc_bwd_kernel<LOGN, FP> : nullptr;
       geom<GBC>(li, GBC::GSCRATCH_FLOATS);
+      li.smem += bwd_dstash_bytes<LOGN, FP>();
       break;
   }
   return li;

@@ -204,6 +204,22 @@ __device__ __forceinline__ void fp_scatter(const float2 (&gl)[8], const float2 (
 }
 
 __device__ __forceinline__ float2 ld_f2(const float* p) { return __ldg(reinterpret_cast<const float2*>(p)); }
+// Activation rows are touched once per launch: optionally streamed (evict-first)
+// so they do not push the L2-prefetched rows out.
+__device__ __forceinline__ float2 ld_row_f2(const float* p) {
+#ifdef ACDC_LD_CS
+  return __ldcs(reinterpret_cast<const float2*>(p));
+#else
+  return __ldg(reinterpret_cast<const float2*>(p));
+#endif
+}
+__device__ __forceinline__ void st_row_f2(float2* p, float2 v) {
+#ifdef ACDC_ST_CS
+  __stcs(p, v);
+#else
+  *p = v;
+#endif
+}
 
 // Pass-0 inputs from two rows (and an optional scale row): the 64-bit pair
 // x[2m], x[2m+1] at m = jsp + q*S (q < 8) holds z[m] (kept) and z[N-1-m]
@@ -218,8 +234,8 @@ __device__ __forceinline__ void fp_load(float2 (&v)[16], const float* xa, const 
   float2 snd[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    float2 a2 = ld_f2(pa + 2 * q * S);
-    float2 b2 = xb ? ld_f2(pb + 2 * q * S) : make_float2(0.f, 0.f);
+    float2 a2 = ld_row_f2(pa + 2 * q * S);
+    float2 b2 = xb ? ld_row_f2(pb + 2 * q * S) : make_float2(0.f, 0.f);
     if constexpr (SCALE) {
       const float2 s2 = ld_f2(ps + 2 * q * S);
       a2 = vmul(a2, s2);
