@@ -191,10 +191,17 @@ def c4(args, dev):
         casc.backward(gy)
         opt.step()  # momentum SGD, zeroes the grads
 
+    def step_fused():  # the SGD update inside each block's gradient reduction (acdc_bwd_sgd_f32)
+        y = casc.forward(x)
+        gy = (2.0 / y.numel()) * (y - target)
+        opt.backward_step(casc, gy)
+
     ms = timeit(step, max(3, args.steps // 10))
+    ms_f = timeit(step_fused, max(3, args.steps // 10))
     return {"config": "C4 deep SELL 32 ACDC layers N=4096 train step (1 GPU of the DP job)", "fused": casc.fused,
             "batch_per_gpu": B, "ms_per_step": ms, "rows_per_s": B / (ms / 1e3),
-            "layer_rows_per_s": B * depth / (ms / 1e3)}
+            "layer_rows_per_s": B * depth / (ms / 1e3),
+            "fused_sgd": {"ms_per_step": ms_f, "rows_per_s": B / (ms_f / 1e3)}}
 
 
 def c5(args, dev):

@@ -29,6 +29,7 @@
  *   afdf_bwd_c64   AfdfLayer.backward (accumulates)  layers.py:206-215
  *   acdc_fft_c64   fft(plan, z) / ifft(plan, z) / kernels.fft_inplace
  *                                                    transforms.py:166-179, _kernels.pyx:18-57
+ *   acdc_bwd_sgd_f32  AcdcLayer.backward + Sgd.step  layers.py:148-156, training.py:58-98
  */
 #ifndef ACDC_B200_H
 #define ACDC_B200_H
@@ -97,6 +98,31 @@ int acdc_bwd_cached_f32(const float* x, const float* dy, float* dx, const float*
                         acdc_stream_t stream);
 
 /* Row-wise orthonormal DCT-II / DCT-III (the reference dct / idct). */
+/* ---- backward fused with the momentum-SGD step of the reference optimizer
+ * (Sgd.step, training.py:58-98) applied to the layer's a, d, bias_d ----
+ * The backward of acdc_bwd_f32 (h2cache NULL: h2 recomputed) or of
+ * acdc_bwd_cached_f32 / cascade_bwd_block_f32 (h2cache set; prev_perm and
+ * prev_relu as for the block backward), whose deterministic gradient
+ * reduction feeds the update instead of storing the gradient:
+ *   g = sum_rows(...) (+ grad_k if accumulate);  v_k <- momentum*v_k - lr_k*(g + weight_decay_k*p_k);
+ *   p_k <- p_k + v_k                                  for k = a, d, bias_d
+ * lr_k = lr_t * lr_mult_k; weight_decay_k = 0 for parameters whose decay flag is
+ * off (the reference's diagonals).  grad_* may be NULL unless accumulate; if
+ * given they are zeroed, like the reference's p.grad[...] = 0.  value[0] and
+ * value[1] are the a and d the backward reads (before the update: stream
+ * order).  The update is computed in fp64 from the fp32 state. */
+typedef struct acdc_sgd_step {
+  float* value[3];        /* a, d, bias_d: [n] fp32, updated in place */
+  float* velocity[3];     /* momentum buffers: [n] fp32 */
+  float lr[3];            /* lr_t * lr_mult per parameter */
+  float weight_decay[3];  /* weight decay, or 0 where decay is off */
+  float momentum;
+} acdc_sgd_step_t;
+int acdc_bwd_sgd_f32(const float* x, const float* dy, float* dx, const float* h2cache, const int32_t* prev_perm,
+                     int prev_relu, float* grad_a, float* grad_d, float* grad_bias, int accumulate,
+                     const acdc_sgd_step_t* step, void* ws, size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx,
+                     int64_t ldy, int64_t lddx, acdc_stream_t stream);
+
 int acdc_dct2_f32(const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream);
 int acdc_dct3_f32(const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream);
 

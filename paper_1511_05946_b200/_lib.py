@@ -26,6 +26,18 @@ ACDC_E_NULL = -6
 
 ABI_VERSION = 1
 
+class SgdStep(ctypes.Structure):
+    """``acdc_sgd_step_t`` (include/acdc_b200.h): one momentum-SGD step of a, d, bias_d."""
+
+    _fields_ = [
+        ("value", ctypes.c_void_p * 3),
+        ("velocity", ctypes.c_void_p * 3),
+        ("lr", ctypes.c_float * 3),
+        ("weight_decay", ctypes.c_float * 3),
+        ("momentum", ctypes.c_float),
+    ]
+
+
 # name -> (restype, argtypes)
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64
@@ -47,6 +59,11 @@ SIGNATURES = {
     "acdc_bwd_cached_f32": (
         ctypes.c_int,
         [_P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _I64, _I32, _I64, _I64, _I64, _P],
+    ),
+    "acdc_bwd_sgd_f32": (
+        ctypes.c_int,
+        [_P, _P, _P, _P, _P, ctypes.c_int, _P, _P, _P, ctypes.c_int, ctypes.POINTER(SgdStep), _P, ctypes.c_size_t,
+         _I64, _I32, _I64, _I64, _I64, _P],
     ),
     "acdc_dct2_f32": (ctypes.c_int, [_P, _P, _I64, _I32, _I64, _I64, _P]),
     "acdc_dct3_f32": (ctypes.c_int, [_P, _P, _I64, _I32, _I64, _I64, _P]),

@@ -703,11 +703,27 @@ __global__ void acdc_n1_bwd_kernel(KParams p) {
   if (threadIdx.x < 3) p.ws[threadIdx.x] = (float)red[threadIdx.x][0];
 }
 
+// Momentum-SGD epilogue of the gradient reduction (reference Sgd.step,
+// training.py:58-98): per parameter k in {a, d, bias_d}
+//   g = grad (+ old grad if accumulating);  v <- mu v - lr_k (g + wd_k p);  p <- p + v
+// with lr_k = lr_t * lr_mult_k and wd_k = 0 for parameters without decay.
+struct SgdDev {
+  float* value[3];
+  float* velocity[3];
+  float lr[3];
+  float wd[3];
+  float momentum;
+};
+
 // grad_c[i] (+)= sum_g ws[g][c][i] in double, in a fixed order: block b owns
 // 32 consecutive outputs; warp s sums groups s, s+8, s+16, ... and the 8 warp
 // partials are added in warp order.  Deterministic for a fixed group count.
+// SGD: the reduced gradient feeds the optimizer step instead of being stored
+// (ga/gd/gb, if given, are zeroed like the reference's p.grad[...] = 0).
+template <bool SGD>
 __global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __restrict__ ws, int64_t groups, int n,
-                                                               float* ga, float* gd, float* gb, int accumulate) {
+                                                               float* ga, float* gd, float* gb, int accumulate,
+                                                               SgdDev sgd) {
   __shared__ double part[8][33];
   const int o = threadIdx.x & 31, s = threadIdx.x >> 5;
   const int64_t total = 3LL * n;
@@ -738,7 +754,18 @@ __global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __re
     for (int k = 0; k < 8; ++k) t += part[k][o];
     float* out = comp == 0 ? ga : (comp == 1 ? gd : gb);
     if (accumulate) t += (double)out[i];
-    out[i] = (float)t;
+    if constexpr (SGD) {
+      float* pv = sgd.value[comp];
+      float* vv = sgd.velocity[comp];
+      const float p0 = pv[i];
+      const double g = t + (double)sgd.wd[comp] * (double)p0;
+      const float v1 = (float)((double)sgd.momentum * (double)vv[i] - (double)sgd.lr[comp] * g);
+      vv[i] = v1;
+      pv[i] = p0 + v1;
+      if (out) out[i] = 0.f;
+    } else {
+      out[i] = (float)t;
+    }
   }
 }
 
@@ -946,12 +973,15 @@ size_t acdc_bwd_workspace_bytes(int64_t rows, int32_t n) {
 static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const float* a, const float* d,
                     const float* h2c, float* grad_a, float* grad_d, float* grad_bias, int accumulate, void* ws,
                     size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, int64_t lddx,
-                    acdc_stream_t stream, const int32_t* epi_perm = nullptr, int epi_relu = 0) {
+                    acdc_stream_t stream, const int32_t* epi_perm = nullptr, int epi_relu = 0,
+                    const SgdDev* sgd = nullptr) {
   if (kind == K_BWD_H2 && rows > 0 && !h2c) return ACDC_E_NULL;
   int rc = check_common(x, dx, rows, n, ldx, lddx);
   if (rc) return rc;
   if (ldy < n) return ACDC_E_SHAPE;
-  if (!a || !d || !grad_a || !grad_d || !grad_bias || (rows > 0 && !dy)) return ACDC_E_NULL;
+  if (!a || !d || (rows > 0 && !dy)) return ACDC_E_NULL;
+  if (!sgd && (!grad_a || !grad_d || !grad_bias)) return ACDC_E_NULL;
+  if (accumulate && (!grad_a || !grad_d || !grad_bias)) return ACDC_E_NULL;
   if (!pair_aligned(n, x, ldx) || !pair_aligned(n, dy, ldy) || !pair_aligned(n, dx, lddx) || !pair_aligned(n, a, 0))
     return ACDC_E_ALIGN;
   int logn;
@@ -975,7 +1005,7 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
   p.ldy = ldy;
   p.ldo = lddx;
   int64_t groups = 1;
-  if (rows == 0) {
+  if (rows == 0 && !sgd) {
     if (!accumulate) {
       cudaMemsetAsync(grad_a, 0, sizeof(float) * n, st);
       cudaMemsetAsync(grad_d, 0, sizeof(float) * n, st);
@@ -984,7 +1014,9 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
   }
-  if (n == 1) {
+  if (rows == 0) {  // zero gradient: the optimizer step still runs (momentum, decay)
+    groups = 0;
+  } else if (n == 1) {
     acdc_n1_bwd_kernel<<<1, 256, 0, st>>>(p);
   } else {
     LaunchInfo li;
@@ -996,8 +1028,12 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
   }
   const int64_t total = 3LL * n;
   int blocks = (int)((total + 31) / 32);
-  acdc_grad_reduce_kernel<<<blocks, 256, 0, st>>>((const float*)ws, groups, n, grad_a, grad_d, grad_bias,
-                                                  accumulate);
+  if (sgd)
+    acdc_grad_reduce_kernel<true><<<blocks, 256, 0, st>>>((const float*)ws, groups, n, grad_a, grad_d, grad_bias,
+                                                          accumulate, *sgd);
+  else
+    acdc_grad_reduce_kernel<false><<<blocks, 256, 0, st>>>((const float*)ws, groups, n, grad_a, grad_d, grad_bias,
+                                                           accumulate, SgdDev{});
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
 }
@@ -1026,6 +1062,29 @@ int cascade_bwd_block_f32(const float* x, const float* dy, float* dx, const floa
   if (prev_perm && dx == dy) return set_error(ACDC_E_SHAPE, "the permuted epilogue cannot write in place");
   return bwd_impl(K_BWD_H2, x, dy, dx, a, d, h2cache, grad_a, grad_d, grad_bias, accumulate, ws, ws_bytes, rows, n,
                   ldx, ldy, lddx, stream, prev_perm, prev_relu);
+}
+
+int acdc_bwd_sgd_f32(const float* x, const float* dy, float* dx, const float* h2cache, const int32_t* prev_perm,
+                     int prev_relu, float* grad_a, float* grad_d, float* grad_bias, int accumulate,
+                     const acdc_sgd_step_t* step, void* ws, size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx,
+                     int64_t ldy, int64_t lddx, acdc_stream_t stream) {
+  if (!step) return ACDC_E_NULL;
+  SgdDev sg;
+  for (int k = 0; k < 3; ++k) {
+    if (!step->value[k] || !step->velocity[k]) return ACDC_E_NULL;
+    sg.value[k] = step->value[k];
+    sg.velocity[k] = step->velocity[k];
+    sg.lr[k] = step->lr[k];
+    sg.wd[k] = step->weight_decay[k];
+  }
+  sg.momentum = step->momentum;
+  if ((prev_perm || prev_relu) && !h2cache)
+    return set_error(ACDC_E_SHAPE, "the block epilogue (prev_perm / prev_relu) needs the h2 cache");
+  if (prev_perm && dx == dy) return set_error(ACDC_E_SHAPE, "the permuted epilogue cannot write in place");
+  if (h2cache && acdc_h2cache_bytes(rows, n) == 0)
+    return set_error(ACDC_E_SIZE, "the h2 cache needs n >= 256 and n <= 16384");
+  return bwd_impl(h2cache ? K_BWD_H2 : K_BWD, x, dy, dx, step->value[0], step->value[1], h2cache, grad_a, grad_d,
+                  grad_bias, accumulate, ws, ws_bytes, rows, n, ldx, ldy, lddx, stream, prev_perm, prev_relu, &sg);
 }
 
 static int transform(int kind, const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy,

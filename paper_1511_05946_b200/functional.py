@@ -12,6 +12,8 @@ Reference counterparts (under /root/reference/pkg/src/acdc):
 
 from __future__ import annotations
 
+import ctypes
+
 import torch
 
 from . import _lib
@@ -19,6 +21,7 @@ from . import _lib
 __all__ = [
     "acdc_forward",
     "acdc_backward",
+    "acdc_backward_sgd",
     "dct",
     "fft",
     "ifft",
@@ -157,6 +160,52 @@ def acdc_backward(
             rc = lib.acdc_bwd_cached_f32(_ptr(x), _ptr(dy), _ptr(dx), _ptr(a), _ptr(d), _ptr(h2cache), _ptr(grad_a),
                                          _ptr(grad_d), _ptr(grad_bias), *common)
         _lib.check(rc)
+    return dx
+
+
+def acdc_backward_sgd(x, dy, params, velocities, lr, weight_decay, momentum, grads=None, accumulate=False, out=None,
+                      h2cache=None, prev_perm=None, prev_relu=False, ws=None) -> torch.Tensor:
+    """Backward of one ACDC layer fused with its momentum-SGD step (reference
+    AcdcLayer.backward + Sgd.step, layers.py:148-156, training.py:58-98).
+
+    ``params`` = (a, d, bias_d) and ``velocities`` are fp32 (n,) CUDA tensors
+    updated in place; ``lr`` / ``weight_decay``: 3 floats (lr_t * lr_mult and
+    the decay actually applied, per parameter).  ``grads`` (grad_a, grad_d,
+    grad_bias) are added to the batch gradient when ``accumulate`` and zeroed.
+    ``h2cache`` / ``prev_perm`` / ``prev_relu`` select the cached and fused-
+    cascade block backward.  Returns dx (computed with the pre-step a, d)."""
+    a = params[0]
+    n = a.shape[0]
+    x = _rows2d(x, n)
+    dy = _rows2d(dy, n, "grad_y")
+    if dy.shape[0] != x.shape[0]:
+        raise ValueError(f"grad_y has {dy.shape[0]} rows, input had {x.shape[0]}")
+    dev = x.device
+    for t in (*params, *velocities, *(grads or ())):
+        if t.device != dev or t.dtype != torch.float32 or not t.is_contiguous() or t.shape != (n,):
+            raise ValueError("parameter, velocity and gradient buffers must be contiguous fp32 (n,) tensors")
+    if accumulate and grads is None:
+        raise ValueError("accumulate=True needs the gradient buffers")
+    dx = torch.empty_like(x, memory_format=torch.contiguous_format) if out is None else out
+    st = _lib.SgdStep()
+    for k in range(3):
+        st.value[k] = params[k].data_ptr()
+        st.velocity[k] = velocities[k].data_ptr()
+        st.lr[k] = float(lr[k])
+        st.weight_decay[k] = float(weight_decay[k])
+    st.momentum = float(momentum)
+    g = grads if grads is not None else (None, None, None)
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        wsb = lib.acdc_bwd_workspace_bytes(max(x.shape[0], 1), n)
+        if wsb == 0:
+            _lib.check(_lib.ACDC_E_CUDA)
+        if ws is None or ws.numel() * 4 < wsb:
+            ws = torch.empty((wsb + 3) // 4, dtype=torch.float32, device=dev)
+        _lib.check(lib.acdc_bwd_sgd_f32(
+            _ptr(x), _ptr(dy), _ptr(dx), _ptr(h2cache), _ptr(prev_perm), 1 if prev_relu else 0, _ptr(g[0]),
+            _ptr(g[1]), _ptr(g[2]), 1 if accumulate else 0, ctypes.byref(st), _ptr(ws), wsb, x.shape[0], n,
+            _ld(x, n), _ld(dy, n), _ld(dx, n), _stream(x)))
     return dx
 
 
@@ -366,12 +415,15 @@ def _ckpt_views(ckpt: torch.Tensor, rows: int, n: int, depth: int):
 
 
 def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor | None, flags,
-                     ckpt: torch.Tensor, grads, accumulate: bool = True) -> torch.Tensor:
+                     ckpt: torch.Tensor, grads, accumulate: bool = True, sgd=None) -> torch.Tensor:
     """Backward of :func:`cascade_forward` (layers.py:341-344): one cached-h2
     block backward per block, last to first, each applying the previous block's
     ReLU mask and inverse permutation in its epilogue.  ``a``, ``d``: sequences
     of (n,) tensors per block; ``grads``: per block (grad_a, grad_d, grad_bias)
-    fp32 (n,) tensors, accumulated in place; ``flags``: host list of ints."""
+    fp32 (n,) tensors, accumulated in place; ``flags``: host list of ints.
+    ``sgd``: optional per-block (params, velocities, lr3, wd3, momentum): each
+    block's momentum-SGD step is fused into its gradient reduction
+    (:func:`acdc_backward_sgd`); the grads are then added in and zeroed."""
     depth = len(a)
     n = a[0].shape[0]
     x = _rows2d(x, n)
@@ -390,6 +442,12 @@ def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor
             pp = perm[l - 1] if (l > 0 and prev & 2) else None
             out = torch.empty_like(g)
             ga, gd, gb = grads[l]
+            if sgd is not None:
+                prm, vel, lr3, wd3, mu = sgd[l]
+                acdc_backward_sgd(xl, g, prm, vel, lr3, wd3, mu, grads=(ga, gd, gb), accumulate=accumulate, out=out,
+                                  h2cache=h2[l], prev_perm=pp, prev_relu=bool(prev & 1), ws=ws)
+                g = out
+                continue
             al, dl = _vec(a[l], n, dev, "a"), _vec(d[l], n, dev, "d")
             _lib.check(lib.cascade_bwd_block_f32(
                 _ptr(xl), _ptr(g), _ptr(out), _ptr(al), _ptr(dl), _ptr(h2[l]), _ptr(pp), 1 if prev & 1 else 0,

@@ -448,8 +448,12 @@ class Cascade:
             x = layer.forward(x)
         return Layer._out(x, host)
 
-    def backward(self, grad_y, retain_cache=False):
+    def backward(self, grad_y, retain_cache=False, sgd=None):
+        """``sgd`` (fused stacks only, from ``training.Sgd.backward_step``): per
+        block SGD specs; each block's optimizer step runs in its backward."""
         host = not (isinstance(grad_y, torch.Tensor) and grad_y.is_cuda)
+        if sgd is not None and self._fused is None:
+            raise ValueError("a fused SGD backward needs a fused cascade")
         if self._fused is not None:
             if self._cache is None:
                 raise RuntimeError("Cascade.backward called before forward")
@@ -460,7 +464,7 @@ class Cascade:
             fz = self._fused
             acdc = [b[0] for b in fz["blocks"]]
             dx = F.cascade_backward(xt, gy, [l.a for l in acdc], [l.d for l in acdc], fz["perm"], fz["flags"], ckpt,
-                                    [(l.grad_a, l.grad_d, l.grad_bias_d) for l in acdc], accumulate=True)
+                                    [(l.grad_a, l.grad_d, l.grad_bias_d) for l in acdc], accumulate=True, sgd=sgd)
             return Layer._out(dx, host)
         g = grad_y
         if host:

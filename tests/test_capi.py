@@ -67,3 +67,22 @@ def test_no_cpu_fallback_in_product():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|\"\"\"[\s\S]*?\"\"\"", "", src), f
+
+
+def test_sgd_entry_validation(lib):
+    """acdc_bwd_sgd_f32 rejects a missing step descriptor and a block epilogue
+    without the h2 cache before any device work."""
+    from paper_1511_05946_b200 import _lib
+
+    f = lib.acdc_bwd_sgd_f32
+    assert f(None, None, None, None, None, 0, None, None, None, 0, None, None, 0, 4, 16, 16, 16, 16, None) == \
+        _lib.ACDC_E_NULL
+    st = _lib.SgdStep()
+    for k in range(3):  # never dereferenced: validation fails first
+        st.value[k] = 0x1000 + 64 * k
+        st.velocity[k] = 0x2000 + 64 * k
+    assert f(None, None, None, None, None, 1, None, None, None, 0, ctypes.byref(st), None, 0, 4, 256, 256, 256, 256,
+             None) == _lib.ACDC_E_SHAPE
+    st.velocity[1] = None
+    assert f(None, None, None, None, None, 0, None, None, None, 0, ctypes.byref(st), None, 0, 4, 256, 256, 256, 256,
+             None) == _lib.ACDC_E_NULL
