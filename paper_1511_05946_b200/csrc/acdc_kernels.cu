@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "kernel_common.cuh"
+#include "tmem.cuh"
 #include "runtime.h"
 
 namespace acdc {
@@ -601,6 +602,222 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
   }
 }
 
+// Cached-h2 backward with its per-thread gradient accumulators in TMEM
+// (tmem.cuh).  With the 48 accumulator floats out of the register file every
+// global load is issued one transform ahead of its use: the h2 block with dy
+// (consumed after the dy transform), the x rows before the g1 transform.  d
+// and a are staged in shared memory once per launch.  Same arithmetic, same
+// per-group partials and the same fixed-order reduction as acdc_bwd_kernel.
+#ifndef ACDC_BWD_TM_CTA
+#define ACDC_BWD_TM_CTA 512
+#endif
+template <int LOGN>
+using GeoBwdTm = Geo<LOGN, 0, fp_gpc<LOGN, ACDC_BWD_TM_CTA>()>;
+// d stash [slot][t] float2 always; the a stash [q][t] float2 only where it fits
+template <int LOGN>
+__host__ __device__ constexpr bool bwd_tm_astash() {
+  using G = GeoBwdTm<LOGN>;
+  return G::SMEM_BYTES + 2 * 8 * G::T * 8 <= G::SMEM_LIMIT;
+}
+template <int LOGN>
+__host__ __device__ constexpr int bwd_tm_stash_bytes() {
+  using G = GeoBwdTm<LOGN>;
+  return (bwd_tm_astash<LOGN>() ? 2 : 1) * 8 * G::T * 8;
+}
+template <int LOGN>
+__host__ __device__ constexpr bool bwd_tm_ok() {
+  using G = GeoBwdTm<LOGN>;
+  // groups must be whole warps: the TMEM accesses are warp-collective and the
+  // groups of one warp could run different row counts
+  return G::FP && G::TW_SMEM && !G::SPLIT && G::T >= 32 && LOGN <= 12 &&  // A/B: slower at n = 8192
+         G::SMEM_BYTES + bwd_tm_stash_bytes<LOGN>() <= G::SMEM_LIMIT && (G::CTA / 32 / 4) * 48 <= 512;
+}
+template <int LOGN>
+__host__ __device__ constexpr int bwd_tm_cols() {
+  using G = GeoBwdTm<LOGN>;
+  constexpr int need = (G::CTA / 32 / 4) * 48;
+  return need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
+}
+
+template <int LOGN>
+__global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
+  using G = GeoBwdTm<LOGN>;
+  constexpr int T = G::T;
+  constexpr int S = FastMap<G>::S;
+  constexpr int COLS = bwd_tm_cols<LOGN>();
+  static_assert(bwd_tm_ok<LOGN>(), "TMEM backward needs the fast-pairing plan");
+  extern __shared__ __align__(16) float smem_f[];
+  __shared__ uint32_t tm_slot;
+  const auto c = group_ctx<G>();
+  const int t = c.t;
+  const int warp = threadIdx.x >> 5;
+  GroupSync<G> gs(c.grp);
+  Xbuf<G> xb{smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS, 0};
+  float2* dst_all = reinterpret_cast<float2*>(smem_f + G::SMEM_BYTES / 4);
+  const float2* dst = dst_all + t;          // [s][t] (d_lo, d_hi)
+  const float2* ast = dst_all + 8 * T + t;  // [q][t] (a[2m], a[2m+1]), m = jsp + q*S
+  const FastMap<G> fm(t, gs.mask);
+  if (c.grp == 0) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      dst_all[t + s * T] = make_float2(__ldg(fm.plo(p.d, s)), __ldg(fm.phi(p.d, s)));
+      if constexpr (bwd_tm_astash<LOGN>()) dst_all[8 * T + t + s * T] = ld_f2(p.a + 2 * (fm.jsp + s * S));
+    }
+  }
+  if (warp == 0) tmem_alloc<COLS>(&tm_slot);
+  tmem_fence_before();
+  const float2 *tw, *cp;
+  stage_tables<G>(p.tab, smem_f, tw, cp);  // __syncthreads: stashes and the TMEM base are published
+  tmem_fence_after();
+  // columns of this thread: [0,16) grad_bias bins, [16,32) grad_d bins, [32,48) grad_a positions
+  const uint32_t ta = tmem_addr(tm_slot, warp, (warp >> 2) * 48);
+  {
+    float z[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) z[i] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) tmem_st8(ta + 8 * k, z);
+  }
+  const int64_t npairs = (p.rows + 1) >> 1;
+  const float2 chi = tab_load<G>(cp, G::N / 2);
+  for (int64_t rp = c.gid; rp < npairs; rp += c.gstride) {
+    const int64_t ra = 2 * rp;
+    const bool hasb = ra + 1 < p.rows;
+    const int64_t rb = hasb ? ra + 1 : ra;
+    if (t == 0 && rp + ACDC_PF_DIST * c.gstride < npairs) {  // a later row pair -> L2
+      const int64_t nr = 2 * (rp + ACDC_PF_DIST * c.gstride);
+      prefetch_row_l2(p.dy + nr * p.ldy, G::N);
+      prefetch_row_l2(p.x + nr * p.ldx, G::N);
+      if (nr + 1 < p.rows) {
+        prefetch_row_l2(p.dy + (nr + 1) * p.ldy, G::N);
+        prefetch_row_l2(p.x + (nr + 1) * p.ldx, G::N);
+      }
+    }
+    // h2 block of this row pair: in flight across the dy transform
+    const float4* hc = reinterpret_cast<const float4*>(p.h2c + rp * 2 * G::N) + t;
+    float4 h2v[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) h2v[s] = __ldcs(hc + s * T);
+    float2 v[16];
+    fp_load<G, false>(v, p.dy + ra * p.ldy, hasb ? p.dy + (ra + 1) * p.ldy : nullptr, nullptr, fm);
+    fft_passes<G, 0>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
+    {
+      float2 w[8], gl[8], gh[8];
+      fp_partner<G>(v, w, fm);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        float ab[8], ad[8];
+        tmem_ld8(ta + 8 * half, ab);
+        tmem_ld8(ta + 16 + 8 * half, ad);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int s = 4 * half + j;
+          const float2 cs = tab_load<G>(fm.plo(cp, s), 0);
+          float2 g3l, g3h;
+          dct2_post(v[s], w[s], cs, fm.special(s), chi, g3l, g3h);
+          ab[2 * j] += g3l.x + g3l.y;
+          ab[2 * j + 1] += g3h.x + g3h.y;
+          const float4 h4 = h2v[s];
+          ad[2 * j] = fmaf(h4.x, g3l.x, fmaf(h4.y, g3l.y, ad[2 * j]));
+          ad[2 * j + 1] = fmaf(h4.z, g3h.x, fmaf(h4.w, g3h.y, ad[2 * j + 1]));
+          const float2 dv = dst[s * T];
+          dct3_pre(vmul(bc(dv.x), g3l), vmul(bc(dv.y), g3h), cs, fm.special(s), chi, gl[s], gh[s]);
+        }
+        tmem_st8(ta + 8 * half, ab);
+        tmem_st8(ta + 16 + 8 * half, ad);
+      }
+      fp_scatter<G>(gl, gh, v, fm);
+    }
+    // x rows of this pair: in flight across the g1 transform
+    float2 xav[8], xbv[8];
+    {
+      const float* pxa = p.x + ra * p.ldx + 2 * fm.jsp;
+      const float* pxb = p.x + rb * p.ldx + 2 * fm.jsp;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        xav[q] = ld_row_f2(pxa + 2 * q * S);
+        xbv[q] = ld_row_f2(pxb + 2 * q * S);  // row rb == ra when !hasb: in bounds, unused
+      }
+    }
+    fft_passes<G, 0>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
+    float2 ga[8], gb[8];
+    fp_out_pairs<G>(v, ga, gb, fm);
+    {
+      float gacc[8];  // positions of q = 0..3, then 4..7
+      const bool relu = p.epi_relu;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        tmem_ld8(ta + 32 + 8 * half, gacc);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int q = 4 * half + j;
+          if (!hasb) xbv[q] = make_float2(0.f, 0.f);
+          const float2 gsum = cadd(make_float2(gacc[2 * j], gacc[2 * j + 1]),
+                                   vfma(gb[q], xbv[q], vmul(ga[q], xav[q])));
+          gacc[2 * j] = gsum.x;
+          gacc[2 * j + 1] = gsum.y;
+          const float2 av = bwd_tm_astash<LOGN>() ? ast[q * T] : ld_f2(p.a + 2 * (fm.jsp + q * S));
+          float2 da = vmul(av, ga[q]);
+          float2 db = vmul(av, gb[q]);
+          if (relu) {  // previous block's ReLU: mask = x > 0 (layers.py:227, 233)
+            da = make_float2(xav[q].x > 0.f ? da.x : 0.f, xav[q].y > 0.f ? da.y : 0.f);
+            db = make_float2(xbv[q].x > 0.f ? db.x : 0.f, xbv[q].y > 0.f ? db.y : 0.f);
+          }
+          ga[q] = da;
+          gb[q] = db;
+        }
+        tmem_st8(ta + 32 + 8 * half, gacc);
+      }
+    }
+    if (p.epi_perm) {  // previous block's permutation: out[perm[j]] = g[j] (layers.py:263-265)
+      float* ra_ = p.y + ra * p.ldo;
+      float* rb_ = p.y + rb * p.ldo;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int* pp = p.epi_perm + 2 * (fm.jsp + q * S);
+        const int j0 = ld_plain_i(pp), j1 = ld_plain_i(pp + 1);
+        ra_[j0] = ga[q].x;
+        ra_[j1] = ga[q].y;
+        if (hasb) {
+          rb_[j0] = gb[q].x;
+          rb_[j1] = gb[q].y;
+        }
+      }
+    } else {
+      float2* oa = reinterpret_cast<float2*>(p.y + ra * p.ldo + 2 * fm.jsp);
+      float2* ob = reinterpret_cast<float2*>(p.y + rb * p.ldo + 2 * fm.jsp);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        st_row_f2(oa + q * S, ga[q]);
+        if (hasb) st_row_f2(ob + q * S, gb[q]);
+      }
+    }
+  }
+  // per-group partials: ws[gid][0] = grad_a, [1] = grad_d, [2] = grad_bias
+  float* wsg = p.ws + c.gid * 3 * G::N;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    float ab[8], ad[8], gacc[8];
+    tmem_ld8(ta + 8 * half, ab);
+    tmem_ld8(ta + 16 + 8 * half, ad);
+    tmem_ld8(ta + 32 + 8 * half, gacc);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int s = 4 * half + j;
+      *fm.plo(wsg + 2 * G::N, s) = ab[2 * j];
+      *fm.phi(wsg + 2 * G::N, s) = ab[2 * j + 1];
+      *fm.plo(wsg + G::N, s) = ad[2 * j];
+      *fm.phi(wsg + G::N, s) = ad[2 * j + 1];
+      wsg[2 * (fm.jsp + s * S)] = gacc[2 * j];
+      wsg[2 * (fm.jsp + s * S) + 1] = gacc[2 * j + 1];
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc<COLS>(tm_slot);
+}
+
 // Row-wise orthonormal DCT-II (transforms.py:137-145) / DCT-III (148-156).
 template <int LOGN>
 __global__ void ACDC_LB(Geo<LOGN>) acdc_dct2_kernel(KParams p) {
@@ -769,6 +986,67 @@ __global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __re
   }
 }
 
+// Two-stage form of the reduction for many groups (small n: thousands of
+// row groups, which one block per 32 outputs would walk serially).  Stage 1:
+// block (x, y) sums groups [64 y, 64 y + 64) of 32 outputs into fp64 chunk
+// partials tmp[y][.] (warp s takes groups s, s+8, ...; warps combined in
+// order).  Stage 2: one thread per output adds the chunks in order, then the
+// same epilogue as acdc_grad_reduce_kernel.  Deterministic for a fixed group
+// count.
+constexpr int RED_CHUNK = 64;
+__global__ void __launch_bounds__(256) acdc_grad_partial_kernel(const float* __restrict__ ws, int64_t groups,
+                                                                int64_t total, double* __restrict__ tmp) {
+  __shared__ double part[8][33];
+  const int o = threadIdx.x & 31, s = threadIdx.x >> 5;
+  const int64_t idx = blockIdx.x * 32LL + o;
+  const int64_t g0 = (int64_t)blockIdx.y * RED_CHUNK;
+  const int64_t g1 = g0 + RED_CHUNK < groups ? g0 + RED_CHUNK : groups;
+  double acc = 0.0;
+  if (idx < total)
+    for (int64_t g = g0 + s; g < g1; g += 8) acc += (double)ws[g * total + idx];
+  part[s][o] = acc;
+  __syncthreads();
+  if (s == 0 && idx < total) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += part[k][o];
+    tmp[(int64_t)blockIdx.y * total + idx] = t;
+  }
+}
+
+template <bool SGD>
+__global__ void __launch_bounds__(256) acdc_grad_final_kernel(const double* __restrict__ tmp, int chunks, int n,
+                                                              float* ga, float* gd, float* gb, int accumulate,
+                                                              SgdDev sgd) {
+  const int64_t total = 3LL * n;
+  const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int comp = (int)(idx / n);
+  const int i = (int)(idx - (int64_t)comp * n);
+  double t = 0.0;
+  for (int c = 0; c < chunks; ++c) t += tmp[(int64_t)c * total + idx];
+  float* out = comp == 0 ? ga : (comp == 1 ? gd : gb);
+  if (accumulate) t += (double)out[i];
+  if constexpr (SGD) {
+    float* pv = sgd.value[comp];
+    float* vv = sgd.velocity[comp];
+    const float p0 = pv[i];
+    const double g = t + (double)sgd.wd[comp] * (double)p0;
+    const float v1 = (float)((double)sgd.momentum * (double)vv[i] - (double)sgd.lr[comp] * g);
+    vv[i] = v1;
+    pv[i] = p0 + v1;
+    if (out) out[i] = 0.f;
+  } else {
+    out[i] = (float)t;
+  }
+}
+
+// fp64 chunk-partial bytes the two-stage reduction needs after the partials.
+static size_t red_tmp_bytes(int64_t groups, int32_t n) {
+  if (groups <= RED_CHUNK) return 0;
+  return (size_t)((groups + RED_CHUNK - 1) / RED_CHUNK) * 3 * (size_t)n * sizeof(double) + 8;
+}
+
 // ---------------------------------------------------------------- host side
 
 enum Kind { K_FWD = 0, K_BWD = 1, K_DCT2 = 2, K_DCT3 = 3, K_FWD_H2 = 4, K_BWD_H2 = 5 };
@@ -814,6 +1092,15 @@ static LaunchInfo info_for(int kind) {
       li.smem += fwd_pstash_bytes<LOGN>();
       break;
     default:
+#ifndef ACDC_NO_BWD_TM
+      if constexpr (bwd_tm_ok<LOGN>()) {
+        li.fn = (const void*)acdc_bwd_tm_kernel<LOGN>;
+        geom<GeoBwdTm<LOGN>>(li, 0);
+        li.smem += bwd_tm_stash_bytes<LOGN>();
+        li.max_per_sm = 512 / bwd_tm_cols<LOGN>();  // resident CTAs must not wait for TMEM columns
+        break;
+      }
+#endif
       li.fn = FP ? (const void*)acdc_bwd_kernel<LOGN, FP> : nullptr;
       geom<GBC>(li, GBC::GSCRATCH_FLOATS);
       li.smem += bwd_dstash_bytes<LOGN, FP>();
@@ -964,7 +1251,8 @@ size_t acdc_bwd_workspace_bytes(int64_t rows, int32_t n) {
     int64_t grid;
     if (launch_info(logn, kind, &li) || !li.fn) continue;
     if (grid_for(li, ((rows > 0 ? rows : 1) + 1) / 2, &grid)) return 0;
-    const size_t b = (size_t)grid * li.gpc * (3 * (size_t)n + (size_t)li.scratch) * sizeof(float);
+    const int64_t groups = grid * li.gpc;
+    const size_t b = (size_t)groups * (3 * (size_t)n + (size_t)li.scratch) * sizeof(float) + red_tmp_bytes(groups, n);
     best = b > best ? b : best;
   }
   return best;
@@ -1004,7 +1292,7 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
   p.ldx = ldx;
   p.ldy = ldy;
   p.ldo = lddx;
-  int64_t groups = 1;
+  int64_t groups = 1, scratch_floats = 0;
   if (rows == 0 && !sgd) {
     if (!accumulate) {
       cudaMemsetAsync(grad_a, 0, sizeof(float) * n, st);
@@ -1023,11 +1311,27 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
     int64_t grid;
     if ((rc = sized(logn, kind, rows, &li, &grid))) return rc;
     groups = grid * li.gpc;
+    scratch_floats = li.scratch;
     p.scratch = p.ws + groups * 3 * (int64_t)n;  // scratch follows the partials
     if ((rc = run(kind, p, n, st))) return rc;
   }
   const int64_t total = 3LL * n;
   int blocks = (int)((total + 31) / 32);
+  if (groups > RED_CHUNK) {
+    const int chunks = (int)((groups + RED_CHUNK - 1) / RED_CHUNK);
+    size_t off = (size_t)groups * (3 * (size_t)n + (size_t)scratch_floats) * sizeof(float);
+    off = (off + 7) & ~(size_t)7;
+    double* tmp = reinterpret_cast<double*>(static_cast<char*>(ws) + off);
+    acdc_grad_partial_kernel<<<dim3(blocks, chunks), 256, 0, st>>>((const float*)ws, groups, total, tmp);
+    const int fb = (int)((total + 255) / 256);
+    if (sgd)
+      acdc_grad_final_kernel<true><<<fb, 256, 0, st>>>(tmp, chunks, n, grad_a, grad_d, grad_bias, accumulate, *sgd);
+    else
+      acdc_grad_final_kernel<false><<<fb, 256, 0, st>>>(tmp, chunks, n, grad_a, grad_d, grad_bias, accumulate,
+                                                        SgdDev{});
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
+  }
   if (sgd)
     acdc_grad_reduce_kernel<true><<<blocks, 256, 0, st>>>((const float*)ws, groups, n, grad_a, grad_d, grad_bias,
                                                           accumulate, *sgd);

@@ -141,6 +141,7 @@ int grid_for(const LaunchInfo& li, int64_t units, int64_t* grid) {
       e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       if (e != cudaSuccess) return set_cuda_error(e);
       if (bps < 1) return set_error(ACDC_E_CUDA, "kernel does not fit on an SM (registers / shared memory)");
+      if (li.max_per_sm > 0 && bps > li.max_per_sm) bps = li.max_per_sm;
       occ = std::make_pair(bps, sms);
       g_occ[key] = occ;
     } else {

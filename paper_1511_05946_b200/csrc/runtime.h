@@ -32,6 +32,7 @@ struct LaunchInfo {
   int gpc = 1;      // row groups per CTA
   int scratch = 0;  // global scratch floats per group
   int smem = 0;     // dynamic shared memory bytes
+  int max_per_sm = 0;  // cap on resident CTAs per SM (TMEM columns), 0 = occupancy only
 };
 
 // Persistent grid: min(CTAs needed for `units` row groups, resident CTAs).
