@@ -23,6 +23,7 @@
 #include <vector>
 
 #include "kernel_common.cuh"
+#include "tma.cuh"
 #include "tmem.cuh"
 #include "runtime.h"
 
@@ -40,6 +41,7 @@ struct KParams {
   float* h2c;         // h2 cache [row pairs][2N] in thread-native layout (H2C kernels)
   const int* epi_perm;  // bwd epilogue (fused cascade): scatter dx through this permutation
   int epi_relu;         // bwd epilogue: zero dx where x <= 0 (the previous block's ReLU)
+  int stage;            // bwd (TMEM kernel): dy rows are 16-byte aligned -> bulk-copy them into smem ahead
   const float2* tab;  // [pass twiddles | c'_k]
   int64_t rows;
   int64_t ldx, ldy, ldo;
@@ -648,11 +650,19 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
   static_assert(bwd_tm_ok<LOGN>(), "TMEM backward needs the fast-pairing plan");
   extern __shared__ __align__(16) float smem_f[];
   __shared__ uint32_t tm_slot;
+  __shared__ __align__(8) uint64_t dy_bar[G::GPC];
   const auto c = group_ctx<G>();
   const int t = c.t;
   const int warp = threadIdx.x >> 5;
   GroupSync<G> gs(c.grp);
   Xbuf<G> xb{smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS, 0};
+  // dy staging: the next row pair's dy rows are bulk-copied into exchange
+  // buffer A (used by exchanges 1 and 3 of an iteration) once exchange 4 has
+  // passed, and read from there at the top of the next iteration.
+  float* stg = smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS;
+  uint64_t* bar = &dy_bar[c.grp];
+  const bool staged = p.stage != 0;
+  if (staged && t == 0) mbar_init(bar, 1);
   float2* dst_all = reinterpret_cast<float2*>(smem_f + G::SMEM_BYTES / 4);
   const float2* dst = dst_all + t;          // [s][t] (d_lo, d_hi)
   const float2* ast = dst_all + 8 * T + t;  // [q][t] (a[2m], a[2m+1]), m = jsp + q*S
@@ -680,6 +690,16 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
   }
   const int64_t npairs = (p.rows + 1) >> 1;
   const float2 chi = tab_load<G>(cp, G::N / 2);
+  auto issue_dy = [&](int64_t r) {  // thread 0 of the group
+    const bool hb = 2 * r + 1 < p.rows;
+    const uint32_t rowb = (uint32_t)G::N * 4u;
+    fence_proxy_async_smem();
+    mbar_expect_tx(bar, hb ? 2u * rowb : rowb);
+    bulk_g2s(stg, p.dy + 2 * r * p.ldy, rowb, bar);
+    if (hb) bulk_g2s(stg + G::N, p.dy + (2 * r + 1) * p.ldy, rowb, bar);
+  };
+  uint32_t parity = 0;
+  if (staged && t == 0 && c.gid < npairs) issue_dy(c.gid);
   for (int64_t rp = c.gid; rp < npairs; rp += c.gstride) {
     const int64_t ra = 2 * rp;
     const bool hasb = ra + 1 < p.rows;
@@ -699,7 +719,21 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
 #pragma unroll
     for (int s = 0; s < 8; ++s) h2v[s] = __ldcs(hc + s * T);
     float2 v[16];
-    fp_load<G, false>(v, p.dy + ra * p.ldy, hasb ? p.dy + (ra + 1) * p.ldy : nullptr, nullptr, fm);
+    if (staged) {
+      mbar_wait(bar, parity);
+      parity ^= 1u;
+      float2 pa[8], pb[8];
+      const float2* sa = reinterpret_cast<const float2*>(stg) + fm.jsp;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        pa[q] = sa[q * S];
+        pb[q] = hasb ? sa[G::N / 2 + q * S] : make_float2(0.f, 0.f);
+      }
+      fp_from_pairs<G>(v, pa, pb, fm);
+      gs.sync();  // buffer A is read by every thread before exchange 1 writes it
+    } else {
+      fp_load<G, false>(v, p.dy + ra * p.ldy, hasb ? p.dy + (ra + 1) * p.ldy : nullptr, nullptr, fm);
+    }
     fft_passes<G, 0>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
     {
       float2 w[8], gl[8], gh[8];
@@ -740,6 +774,8 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
       }
     }
     fft_passes<G, 0>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
+    // exchange 4 has passed: buffer A (last read at exchange 3) takes the next dy
+    if (staged && t == 0 && rp + c.gstride < npairs) issue_dy(rp + c.gstride);
     float2 ga[8], gb[8];
     fp_out_pairs<G>(v, ga, gb, fm);
     {
@@ -1288,6 +1324,11 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
   p.h2c = const_cast<float*>(h2c);
   p.epi_perm = epi_perm;
   p.epi_relu = epi_relu;
+#ifdef ACDC_NO_STAGE
+  p.stage = 0;
+#else
+  p.stage = (((uintptr_t)dy & 15) == 0 && (ldy & 3) == 0) ? 1 : 0;
+#endif
   p.rows = rows;
   p.ldx = ldx;
   p.ldy = ldy;

@@ -257,11 +257,14 @@ struct Plan {
 // hold GPC row-pair groups (512 threads when T <= 512) sharing one copy of the
 // tables; the plan prefers tables in smem and double-buffered exchanges and
 // falls back (single buffer, tables in global) until the CTA fits in 227 KB.
+#ifndef ACDC_E32_FROM  // log2 N from which each thread holds 32 values (T = N / 32)
+#define ACDC_E32_FROM 15
+#endif
 template <int LOGN, int STASH = 0, int GPCX = 0>
 struct Geo : Plan<LOGN> {
   using P_ = Plan<LOGN>;
   static constexpr int N = 1 << LOGN;
-  static constexpr int E = LOGN >= 15 ? 32 : (N >= 16 ? 16 : N);  // complex values per thread
+  static constexpr int E = LOGN >= ACDC_E32_FROM ? 32 : (N >= 16 ? 16 : N);  // complex values per thread
   static constexpr int T = N / E;                                 // threads per row-pair group
   static constexpr int GPC = GPCX ? GPCX : (T <= 512 ? 512 / T : 1);  // groups per CTA
   static constexpr int CTA = T * GPC;                             // threads per CTA
