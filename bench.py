@@ -229,7 +229,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1511_05946_b200 import functional as F
+    from paper_1511_05946_b200 import _lib, functional as F
 
     world, rank, local = dist_setup(args.gpus)
     n, B = args.n, args.batch
@@ -379,7 +379,9 @@ def run_ours(args):
                 "allreduce_ms": ar_ms,
             },
             "clocks": clocks,
-            "gpu_launches": 3 * args.steps,  # fwd + bwd + grad reduce per step (this arm's timed region)
+            # fwd + bwd + its one- or two-stage grad reduction per step (this arm's timed region)
+            "gpu_launches": (1 + _lib.load().acdc_bwd_launch_count(B, n, 1 if best["mode"] == "h2cache" else 0))
+            * args.steps,
             "e2e": e2e,
             "dense_cublas": dense,
         }

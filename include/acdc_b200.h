@@ -71,6 +71,10 @@ int acdc_fwd_f32(const float* x, float* y, const float* a, const float* d, const
 /* Bytes of scratch acdc_bwd_f32 needs for (rows, n) on the current device
  * (per-group gradient partials; 0 on error). */
 size_t acdc_bwd_workspace_bytes(int64_t rows, int32_t n);
+/* Kernels one backward call launches for this shape (the backward plus its one-
+ * or two-stage gradient reduction); cached != 0 for the h2-cache backward.
+ * -1 on invalid arguments. */
+int acdc_bwd_launch_count(int64_t rows, int32_t n, int cached);
 
 /* Backward of acdc_fwd_f32 (layers.py:148-156), h2 recomputed:
  *   g3 = C2(dy); g1 = C3(d * g3); dx = a * g1

@@ -50,6 +50,7 @@ SIGNATURES = {
     "acdc_prepare": (ctypes.c_int, [_I32]),
     "acdc_fwd_f32": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I32, _I64, _I64, _P]),
     "acdc_bwd_workspace_bytes": (ctypes.c_size_t, [_I64, _I32]),
+    "acdc_bwd_launch_count": (ctypes.c_int, [_I64, _I32, ctypes.c_int]),
     "acdc_bwd_f32": (
         ctypes.c_int,
         [_P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _I64, _I32, _I64, _I64, _I64, _P],

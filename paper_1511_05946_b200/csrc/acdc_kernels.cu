@@ -1294,6 +1294,17 @@ size_t acdc_bwd_workspace_bytes(int64_t rows, int32_t n) {
   return best;
 }
 
+int acdc_bwd_launch_count(int64_t rows, int32_t n, int cached) {
+  int logn;
+  if (check_n(n, &logn) || rows < 0) return -1;
+  if (rows == 0) return 0;
+  if (logn == 0) return 2;
+  LaunchInfo li;
+  int64_t grid;
+  if (sized(logn, cached ? K_BWD_H2 : K_BWD, rows, &li, &grid)) return -1;
+  return grid * li.gpc > RED_CHUNK ? 3 : 2;  // backward + one or two reduction kernels
+}
+
 static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const float* a, const float* d,
                     const float* h2c, float* grad_a, float* grad_d, float* grad_bias, int accumulate, void* ws,
                     size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, int64_t lddx,

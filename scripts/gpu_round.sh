@@ -12,10 +12,10 @@ if [ "$TESTS" = "1" ]; then
 fi
 timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 cat gpurun_out/${TAG}_bench.json; tail -3 gpurun_out/${TAG}_bench.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file gpurun_out/${TAG}_launches.csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/${TAG}_launches.csv \
   python bench.py --steps 5 --warmup 3 --mode h2cache --no-cpu-baseline --no-e2e --no-dense > /dev/null 2>&1
 if [ "$FULL" = "1" ]; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:acdc_ -s 6 -c 3 -o gpurun_out/${TAG}_prof \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:acdc_ -s 8 -c 4 -o gpurun_out/${TAG}_prof \
     python bench.py --steps 3 --warmup 3 --mode h2cache --no-cpu-baseline --no-e2e --no-dense > gpurun_out/${TAG}_ncu.log 2>&1
   tail -2 gpurun_out/${TAG}_ncu.log
 fi
