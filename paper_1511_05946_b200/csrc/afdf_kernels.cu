@@ -19,6 +19,7 @@
 
 #include "fft_engine.cuh"
 #include "runtime.h"
+#include "tmem.cuh"
 
 namespace acdc {
 
@@ -249,6 +250,148 @@ __global__ void ACDC_LB(GeoF<LOGN>) afdf_bwd_kernel(FParams p) {
     }
 }
 
+// Backward with its per-thread state in TMEM (tmem.cuh): conj(h2), the x row
+// (read once instead of twice), and the grad_a / grad_d partials, 128 columns
+// per thread.  a is staged in shared memory once per launch; dy is loaded
+// before the h2 transform and consumed after it.  Needs R_first == R_last
+// (each thread owns positions t + q T in every stage), E = 16 and whole-warp
+// groups.  Same partials and fixed-order reduction as afdf_bwd_kernel.
+template <int LOGN>
+using GeoFT = Geo<LOGN>;
+// smem: pass twiddles (no DCT table), two exchange buffers per group, a stash
+template <int LOGN>
+__host__ __device__ constexpr int afdf_tm_tab_floats() {
+  return (2 * GeoFT<LOGN>::TW_ENTRIES + 3) & ~3;
+}
+template <int LOGN>
+__host__ __device__ constexpr int afdf_tm_smem() {
+  using G = GeoFT<LOGN>;
+  return 4 * (afdf_tm_tab_floats<LOGN>() + G::GPC * 2 * G::BUF_FLOATS) + 16 * G::T * 8;
+}
+template <int LOGN>
+__host__ __device__ constexpr bool afdf_tm_ok() {
+  using G = GeoFT<LOGN>;
+  return G::E == 16 && G::T >= 32 && G::NPASS >= 2 && G::radix(0) == 16 && G::radix(G::NPASS - 1) == 16 &&
+         G::TW_SMEM && G::NBUF == 2 && !G::SPLIT && afdf_tm_smem<LOGN>() <= G::SMEM_LIMIT &&
+         (G::CTA / 32 / 4) * 128 <= 512;
+}
+
+template <int LOGN>
+__global__ void ACDC_LB(GeoFT<LOGN>) afdf_bwd_tm_kernel(FParams p) {
+  using G = GeoFT<LOGN>;
+  constexpr int T = G::T;
+  static_assert(afdf_tm_ok<LOGN>(), "TMEM AFDF backward plan");
+  extern __shared__ __align__(16) float smem_f[];
+  __shared__ uint32_t tm_slot;
+  const int grp = threadIdx.x / T, t = threadIdx.x % T;
+  const int warp = threadIdx.x >> 5;
+  const int64_t gid = (int64_t)blockIdx.x * G::GPC + grp, gstride = (int64_t)gridDim.x * G::GPC;
+  GroupSync<G> gs(grp);
+  constexpr int TABF = afdf_tm_tab_floats<LOGN>();
+  Xbuf<G> xb{smem_f + TABF + grp * 2 * G::BUF_FLOATS, 0};
+  float2* ast = reinterpret_cast<float2*>(smem_f + TABF + G::GPC * 2 * G::BUF_FLOATS) + t;  // [q][t] a at t + q T
+  if (grp == 0) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) ast[q * T] = __ldg(p.a + t + q * T);
+  }
+  if (warp == 0) tmem_alloc<512>(&tm_slot);
+  tmem_fence_before();
+  const float2* tw;
+  f_stage_tables<G>(p, smem_f, tw);  // __syncthreads: the a stash and the TMEM base are published
+  tmem_fence_after();
+  // columns: [0,32) conj(h2), [32,64) x, [64,96) grad_a partials, [96,128) grad_d partials
+  const uint32_t ta = tmem_addr(tm_slot, warp, (warp >> 2) * 128);
+  {
+    float2 z[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) z[i] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 4; k < 8; ++k) tmem_st16(ta + 16 * k, z);
+  }
+  const float scale = 1.0f / G::N;
+  for (int64_t r = gid; r < p.rows; r += gstride) {
+    const float2* xr = p.x + r * p.ldx + t;
+    const float2* dyr = p.dy + r * p.ldy + t;
+    float2 v[16], g[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = __ldg(xr + q * T);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) g[q] = __ldg(dyr + q * T);  // in flight across the h2 transform
+    {
+      float2 h[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) h[q] = v[q];
+      tmem_st16(ta + 32, h);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) h[q] = v[8 + q];
+      tmem_st16(ta + 48, h);
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = cmul(v[q], ast[q * T]);
+    fft_passes<G>(v, xb, gs, tw, t);  // h2 = FFT(a x)
+    {
+      float2 h[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) h[q] = conjf2(v[q]);
+      tmem_st16(ta + 0, h);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) h[q] = conjf2(v[8 + q]);
+      tmem_st16(ta + 16, h);
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = g[q];
+    fft_passes<G>(v, xb, gs, tw, t);  // g = FFT(dy)
+    // grad_d partial += g * conj(h2);  V = conj(g) * d
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      float2 h[8], ad[8];
+      tmem_ld16(ta + 16 * half, h);
+      tmem_ld16(ta + 96 + 16 * half, ad);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int q = 8 * half + j;
+        ad[j] = cadd(ad[j], cmul(v[q], h[j]));
+        v[q] = cmul(conjf2(v[q]), ld_param(p.d + t + q * T));
+      }
+      tmem_st16(ta + 96 + 16 * half, ad);
+    }
+    fft_passes<G>(v, xb, gs, tw, t);  // g1 = conj(FFT(V)) / N  (times N: the 1/N cancels, see header)
+    float2* oxr = p.y + r * p.ldo + t;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      float2 xv[8], ga[8];
+      tmem_ld16(ta + 32 + 16 * half, xv);
+      tmem_ld16(ta + 64 + 16 * half, ga);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int q = 8 * half + j;
+        const float2 g1 = make_float2(v[q].x * scale, -v[q].y * scale);
+        ga[j] = cadd(ga[j], cmul_conj(g1, xv[j]));
+        oxr[q * T] = cmul_conj(g1, ast[q * T]);
+      }
+      tmem_st16(ta + 64 + 16 * half, ga);
+    }
+  }
+  // partials: ws[gid][0] = grad_a, [1] = grad_d (times 1/N)
+  float2* w = p.ws + gid * 2 * G::N + t;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    float2 ga[8], ad[8];
+    tmem_ld16(ta + 64 + 16 * half, ga);
+    tmem_ld16(ta + 96 + 16 * half, ad);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int q = 8 * half + j;
+      w[q * T] = ga[j];
+      w[G::N + q * T] = make_float2(ad[j].x * scale, ad[j].y * scale);
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc<512>(tm_slot);
+}
+
 // out_k[i] (+)= sum_g ws[g][k][i] (k < 2 complex outputs of length n), in double,
 // fixed order (same scheme as acdc_grad_reduce_kernel).
 __global__ void __launch_bounds__(256) afdf_grad_reduce_kernel(const float* __restrict__ ws, int64_t groups, int n,
@@ -301,6 +444,16 @@ static LaunchInfo finfo(int kind) {
   li.gpc = G::GPC;
   li.scratch = bwd ? GB::GSCRATCH_FLOATS : 0;
   li.smem = bwd ? GB::SMEM_BYTES : G::SMEM_BYTES;
+#ifndef ACDC_NO_AFDF_TM
+  if constexpr (afdf_tm_ok<LOGN>()) {
+    if (bwd) {
+      li.fn = (const void*)afdf_bwd_tm_kernel<LOGN>;
+      li.scratch = 0;
+      li.smem = afdf_tm_smem<LOGN>();
+      li.max_per_sm = 1;  // 512 TMEM columns per CTA
+    }
+  }
+#endif
   return li;
 }
 
