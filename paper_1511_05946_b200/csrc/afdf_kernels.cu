@@ -128,6 +128,105 @@ __global__ void ACDC_LB(Geo<LOGN>) afdf_fwd_kernel(FParams p) {
   }
 }
 
+template <int LOGN>
+using GeoFT = Geo<LOGN>;
+// smem: pass twiddles (no DCT table), two exchange buffers per group, a stash
+template <int LOGN>
+__host__ __device__ constexpr int afdf_tm_tab_floats() {
+  return (2 * GeoFT<LOGN>::TW_ENTRIES + 3) & ~3;
+}
+template <int LOGN>
+__host__ __device__ constexpr int afdf_tm_smem() {
+  using G = GeoFT<LOGN>;
+  return 4 * (afdf_tm_tab_floats<LOGN>() + G::GPC * 2 * G::BUF_FLOATS) + 16 * G::T * 8;
+}
+template <int LOGN>
+__host__ __device__ constexpr bool afdf_tm_ok() {
+  using G = GeoFT<LOGN>;
+  return G::E == 16 && G::T >= 32 && G::NPASS >= 2 && G::radix(0) == 16 && G::radix(G::NPASS - 1) == 16 &&
+         G::TW_SMEM && G::NBUF == 2 && !G::SPLIT && afdf_tm_smem<LOGN>() <= G::SMEM_LIMIT &&
+         (G::CTA / 32 / 4) * 128 <= 512;
+}
+
+// Forward with a and d held in TMEM (64 columns per thread, loaded once per
+// launch) instead of 32 global loads per row, and the next row's x loaded
+// into registers across the second transform.  Same plan conditions as the
+// TMEM backward.
+template <int LOGN>
+__host__ __device__ constexpr int afdf_tmf_smem() {
+  using G = GeoFT<LOGN>;
+  return 4 * (afdf_tm_tab_floats<LOGN>() + G::GPC * 2 * G::BUF_FLOATS);
+}
+
+template <int LOGN>
+__global__ void ACDC_LB(GeoFT<LOGN>) afdf_fwd_tm_kernel(FParams p) {
+  using G = GeoFT<LOGN>;
+  constexpr int T = G::T;
+  static_assert(afdf_tm_ok<LOGN>(), "TMEM AFDF plan");
+  extern __shared__ __align__(16) float smem_f[];
+  __shared__ uint32_t tm_slot;
+  const int grp = threadIdx.x / T, t = threadIdx.x % T;
+  const int warp = threadIdx.x >> 5;
+  const int64_t gid = (int64_t)blockIdx.x * G::GPC + grp, gstride = (int64_t)gridDim.x * G::GPC;
+  GroupSync<G> gs(grp);
+  constexpr int TABF = afdf_tm_tab_floats<LOGN>();
+  Xbuf<G> xb{smem_f + TABF + grp * 2 * G::BUF_FLOATS, 0};
+  if (warp == 0) tmem_alloc<256>(&tm_slot);
+  tmem_fence_before();
+  const float2* tw;
+  f_stage_tables<G>(p, smem_f, tw);
+  tmem_fence_after();
+  // columns [0,32) a, [32,64) d at positions t + q T
+  const uint32_t ta = tmem_addr(tm_slot, warp, (warp >> 2) * 64);
+  {
+    float2 h[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2* src = (k < 2 ? p.a : p.d) + t + (k & 1) * 8 * T;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) h[j] = __ldg(src + j * T);
+      tmem_st16(ta + 16 * k, h);
+    }
+  }
+  const float scale = 1.0f / G::N;
+  float2 xn[16];
+  if (gid < p.rows) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) xn[q] = __ldg(p.x + gid * p.ldx + t + q * T);
+  }
+  for (int64_t r = gid; r < p.rows; r += gstride) {
+    float2 v[16];
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      float2 av[8];
+      tmem_ld16(ta + 16 * half, av);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[8 * half + j] = cmul(xn[8 * half + j], av[j]);
+    }
+    fft_passes<G>(v, xb, gs, tw, t);
+    // V = conj(d * X)
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      float2 dv[8];
+      tmem_ld16(ta + 32 + 16 * half, dv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[8 * half + j] = conjf2(cmul(v[8 * half + j], dv[j]));
+    }
+    if (r + gstride < p.rows) {  // next row: in flight across the inverse transform
+#pragma unroll
+      for (int q = 0; q < 16; ++q) xn[q] = __ldg(p.x + (r + gstride) * p.ldx + t + q * T);
+    }
+    fft_passes<G>(v, xb, gs, tw, t);
+    float2* yr = p.y + r * p.ldo + t;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) yr[q * T] = make_float2(v[q].x * scale, -v[q].y * scale);
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc<256>(tm_slot);
+}
+
 // Row-wise complex DFT (transforms.py:166-179, _kernels.pyx:18-57): forward
 // unnormalised, inverse = conj(FFT(conj z)) / N.  Reads a whole row into
 // registers before writing, so z == out (in place) is allowed.
@@ -256,26 +355,6 @@ __global__ void ACDC_LB(GeoF<LOGN>) afdf_bwd_kernel(FParams p) {
 // before the h2 transform and consumed after it.  Needs R_first == R_last
 // (each thread owns positions t + q T in every stage), E = 16 and whole-warp
 // groups.  Same partials and fixed-order reduction as afdf_bwd_kernel.
-template <int LOGN>
-using GeoFT = Geo<LOGN>;
-// smem: pass twiddles (no DCT table), two exchange buffers per group, a stash
-template <int LOGN>
-__host__ __device__ constexpr int afdf_tm_tab_floats() {
-  return (2 * GeoFT<LOGN>::TW_ENTRIES + 3) & ~3;
-}
-template <int LOGN>
-__host__ __device__ constexpr int afdf_tm_smem() {
-  using G = GeoFT<LOGN>;
-  return 4 * (afdf_tm_tab_floats<LOGN>() + G::GPC * 2 * G::BUF_FLOATS) + 16 * G::T * 8;
-}
-template <int LOGN>
-__host__ __device__ constexpr bool afdf_tm_ok() {
-  using G = GeoFT<LOGN>;
-  return G::E == 16 && G::T >= 32 && G::NPASS >= 2 && G::radix(0) == 16 && G::radix(G::NPASS - 1) == 16 &&
-         G::TW_SMEM && G::NBUF == 2 && !G::SPLIT && afdf_tm_smem<LOGN>() <= G::SMEM_LIMIT &&
-         (G::CTA / 32 / 4) * 128 <= 512;
-}
-
 template <int LOGN>
 __global__ void ACDC_LB(GeoFT<LOGN>) afdf_bwd_tm_kernel(FParams p) {
   using G = GeoFT<LOGN>;
@@ -446,6 +525,13 @@ static LaunchInfo finfo(int kind) {
   li.smem = bwd ? GB::SMEM_BYTES : G::SMEM_BYTES;
 #ifndef ACDC_NO_AFDF_TM
   if constexpr (afdf_tm_ok<LOGN>()) {
+#ifndef ACDC_NO_AFDF_TMF
+    if (kind == 0) {
+      li.fn = (const void*)afdf_fwd_tm_kernel<LOGN>;
+      li.smem = afdf_tmf_smem<LOGN>();
+      li.max_per_sm = 2;  // 256 TMEM columns per CTA
+    }
+#endif
     if (bwd) {
       li.fn = (const void*)afdf_bwd_tm_kernel<LOGN>;
       li.scratch = 0;
