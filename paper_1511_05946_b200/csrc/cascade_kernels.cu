@@ -70,18 +70,26 @@ __global__ void ACDC_LB(Geo<LOGN>) cascade_fwd_kernel(CParams p) {
         pb[q] = hasb ? ld_f2(xbr + 2 * q * S) : make_float2(0.f, 0.f);
       }
     }
+    float2 an[8];  // a_l at this thread's position pairs (issued one block ahead)
+    {
+      const float* pav = p.a + 2 * fm.jsp;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) an[q] = ld_f2(pav + 2 * q * S);
+    }
     for (int l = 0; l < p.depth; ++l) {
-      const float* al = p.a + (int64_t)l * N;
       const float* dl = p.d + (int64_t)l * N;
       const float* bl = p.bias + (int64_t)l * N;
+      // d_l / bias_l of this thread's spectral slots: in flight across the first transform
+      float4 dbv[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        dbv[s] = make_float4(__ldg(fm.plo(dl, s)), __ldg(fm.phi(dl, s)), __ldg(fm.plo(bl, s)), __ldg(fm.phi(bl, s)));
       float2 v[16];
       {
-        const float* pav = al + 2 * fm.jsp;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const float2 s2 = ld_plain_f2(pav + 2 * q * S);
-          pa[q] = vmul(pa[q], s2);
-          pb[q] = vmul(pb[q], s2);
+          pa[q] = vmul(pa[q], an[q]);
+          pb[q] = vmul(pb[q], an[q]);
         }
         fp_from_pairs<G>(v, pa, pb, fm);
       }
@@ -96,13 +104,16 @@ __global__ void ACDC_LB(Geo<LOGN>) cascade_fwd_kernel(CParams p) {
           float2 xl, xh;
           dct2_post(v[s], w[s], cs, fm.special(s), chi, xl, xh);
           __stcs(hc + s * T, make_float4(xl.x, xl.y, xh.x, xh.y));
-          const float dlo = ld_plain(fm.plo(dl, s)), blo = ld_plain(fm.plo(bl, s));
-          const float dhi = ld_plain(fm.phi(dl, s)), bhi = ld_plain(fm.phi(bl, s));
-          xl = vfma(xl, bc(dlo), bc(blo));
-          xh = vfma(xh, bc(dhi), bc(bhi));
+          xl = vfma(xl, bc(dbv[s].x), bc(dbv[s].z));
+          xh = vfma(xh, bc(dbv[s].y), bc(dbv[s].w));
           dct3_pre(xl, xh, cs, fm.special(s), chi, gl[s], gh[s]);
         }
         fp_scatter<G>(gl, gh, v, fm);
+      }
+      if (l + 1 < p.depth) {  // a_{l+1}: in flight across the second transform
+        const float* pav = p.a + (int64_t)(l + 1) * N + 2 * fm.jsp;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) an[q] = ld_f2(pav + 2 * q * S);
       }
       fft_passes<G, 0>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
       fp_out_pairs<G>(v, pa, pb, fm);  // ACDC_l output pairs
