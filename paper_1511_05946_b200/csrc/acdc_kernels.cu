@@ -829,14 +829,47 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
       }
     }
   }
-  // per-group partials: ws[gid][0] = grad_a, [1] = grad_d, [2] = grad_bias
-  float* wsg = p.ws + c.gid * 3 * G::N;
+  // One partial per CTA: groups 1.. park their 48 accumulator columns in
+  // their own (now idle) exchange buffers, group 0 adds them in group order.
+  // ws[cta][0] = grad_a, [1] = grad_d, [2] = grad_bias.
+  if constexpr (G::GPC > 1) {
+    static_assert(48 * T <= G::NBUF * G::BUF_FLOATS, "parking area");
+    float* park = smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS + t;  // [col][T]
+    if (c.grp > 0) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        float u[8];
+        tmem_ld8(ta + 8 * k, u);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) park[(8 * k + i) * T] = u[i];
+      }
+    }
+    __syncthreads();
+    if (c.grp > 0) {
+      tmem_fence_before();
+      __syncthreads();
+      tmem_fence_after();
+      if (warp == 0) tmem_dealloc<COLS>(tm_slot);
+      return;
+    }
+  }
+  float* wsg = p.ws + (int64_t)blockIdx.x * 3 * G::N;
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     float ab[8], ad[8], gacc[8];
     tmem_ld8(ta + 8 * half, ab);
     tmem_ld8(ta + 16 + 8 * half, ad);
     tmem_ld8(ta + 32 + 8 * half, gacc);
+#pragma unroll
+    for (int g = 1; g < G::GPC; ++g) {
+      const float* park = smem_f + G::TAB_FLOATS + g * G::GROUP_FLOATS + t;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        ab[i] += park[(8 * half + i) * T];
+        ad[i] += park[(16 + 8 * half + i) * T];
+        gacc[i] += park[(32 + 8 * half + i) * T];
+      }
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int s = 4 * half + j;
@@ -1024,12 +1057,12 @@ __global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __re
 
 // Two-stage form of the reduction for many groups (small n: thousands of
 // row groups, which one block per 32 outputs would walk serially).  Stage 1:
-// block (x, y) sums groups [64 y, 64 y + 64) of 32 outputs into fp64 chunk
+// block (x, y) sums groups [RED_CHUNK y, RED_CHUNK (y + 1)) of 32 outputs into fp64 chunk
 // partials tmp[y][.] (warp s takes groups s, s+8, ...; warps combined in
 // order).  Stage 2: one thread per output adds the chunks in order, then the
 // same epilogue as acdc_grad_reduce_kernel.  Deterministic for a fixed group
 // count.
-constexpr int RED_CHUNK = 64;
+constexpr int RED_CHUNK = 160;
 __global__ void __launch_bounds__(256) acdc_grad_partial_kernel(const float* __restrict__ ws, int64_t groups,
                                                                 int64_t total, double* __restrict__ tmp) {
   __shared__ double part[8][33];
@@ -1132,6 +1165,7 @@ static LaunchInfo info_for(int kind) {
       if constexpr (bwd_tm_ok<LOGN>()) {
         li.fn = (const void*)acdc_bwd_tm_kernel<LOGN>;
         geom<GeoBwdTm<LOGN>>(li, 0);
+        li.red_per_cta = 1;  // the CTA's groups are pre-reduced in shared memory
         li.smem += bwd_tm_stash_bytes<LOGN>();
         li.max_per_sm = 512 / bwd_tm_cols<LOGN>();  // resident CTAs must not wait for TMEM columns
         break;
@@ -1287,7 +1321,7 @@ size_t acdc_bwd_workspace_bytes(int64_t rows, int32_t n) {
     int64_t grid;
     if (launch_info(logn, kind, &li) || !li.fn) continue;
     if (grid_for(li, ((rows > 0 ? rows : 1) + 1) / 2, &grid)) return 0;
-    const int64_t groups = grid * li.gpc;
+    const int64_t groups = grid * (li.red_per_cta ? li.red_per_cta : li.gpc);
     const size_t b = (size_t)groups * (3 * (size_t)n + (size_t)li.scratch) * sizeof(float) + red_tmp_bytes(groups, n);
     best = b > best ? b : best;
   }
@@ -1302,7 +1336,7 @@ int acdc_bwd_launch_count(int64_t rows, int32_t n, int cached) {
   LaunchInfo li;
   int64_t grid;
   if (sized(logn, cached ? K_BWD_H2 : K_BWD, rows, &li, &grid)) return -1;
-  return grid * li.gpc > RED_CHUNK ? 3 : 2;  // backward + one or two reduction kernels
+  return grid * (li.red_per_cta ? li.red_per_cta : li.gpc) > RED_CHUNK ? 3 : 2;  // backward + one or two reduction kernels
 }
 
 static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const float* a, const float* d,
@@ -1362,7 +1396,7 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
     LaunchInfo li;
     int64_t grid;
     if ((rc = sized(logn, kind, rows, &li, &grid))) return rc;
-    groups = grid * li.gpc;
+    groups = grid * (li.red_per_cta ? li.red_per_cta : li.gpc);
     scratch_floats = li.scratch;
     p.scratch = p.ws + groups * 3 * (int64_t)n;  // scratch follows the partials
     if ((rc = run(kind, p, n, st))) return rc;
