@@ -613,6 +613,9 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
 #ifndef ACDC_BWD_TM_CTA
 #define ACDC_BWD_TM_CTA 512
 #endif
+#ifndef ACDC_TM_MAX_LOGN  // largest size with tables in smem (n = 16384 keeps them in global memory)
+#define ACDC_TM_MAX_LOGN 13
+#endif
 template <int LOGN>
 using GeoBwdTm = Geo<LOGN, 0, fp_gpc<LOGN, ACDC_BWD_TM_CTA>()>;
 // d stash [slot][t] float2 always; the a stash [q][t] float2 only where it fits
@@ -631,7 +634,7 @@ __host__ __device__ constexpr bool bwd_tm_ok() {
   using G = GeoBwdTm<LOGN>;
   // groups must be whole warps: the TMEM accesses are warp-collective and the
   // groups of one warp could run different row counts
-  return G::FP && G::TW_SMEM && !G::SPLIT && G::T >= 32 && LOGN <= 12 &&  // A/B: slower at n = 8192
+  return G::FP && G::TW_SMEM && !G::SPLIT && G::T >= 32 && LOGN <= ACDC_TM_MAX_LOGN &&
          G::SMEM_BYTES + bwd_tm_stash_bytes<LOGN>() <= G::SMEM_LIMIT && (G::CTA / 32 / 4) * 48 <= 512;
 }
 template <int LOGN>
