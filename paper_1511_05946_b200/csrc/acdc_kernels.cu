@@ -353,9 +353,6 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
           prefetch_row_l2(p.dy + (nr + 1) * p.ldy, G::N);
           prefetch_row_l2(p.x + (nr + 1) * p.ldx, G::N);
         }
-#ifdef ACDC_PF_H2
-        if constexpr (H2C) prefetch_row_l2(p.h2c + nrp * 2 * G::N, 2 * G::N);
-#endif
       }
       float2 v[16];
       const float2 chi = tab_load<G>(cp, G::N / 2);
@@ -433,18 +430,6 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
       }  // !H2C
       // g1 = C3(d * g3); dx = a * g1; grad_a partial += x * g1
       const int64_t rb = hasb ? ra + 1 : ra;
-#ifdef ACDC_BWD_XPRE  // experiment: x loads in flight across the last FFT
-      float2 xav[8], xbv[8];
-      {
-        const float* pxa = xa + 2 * fm.jsp;
-        const float* pxb = p.x + rb * p.ldx + 2 * fm.jsp;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          xav[q] = ld_row_f2(pxa + 2 * q * S);
-          xbv[q] = ld_row_f2(pxb + 2 * q * S);
-        }
-      }
-#endif
       fft_passes<G, 0>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
       float2 ga[8], gb[8];
       fp_out_pairs<G>(v, ga, gb, fm);
@@ -456,14 +441,12 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
       // All x / a loads of the row pair are issued before any store or
       // volatile index load, so their L2 latencies overlap instead of
       // serialising once per q.
-#ifndef ACDC_BWD_XPRE
       float2 xav[8], xbv[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         xav[q] = ld_row_f2(pxa + 2 * q * S);
         xbv[q] = ld_row_f2(pxb + 2 * q * S);  // row rb == ra when !hasb: in bounds, unused
       }
-#endif
       const bool relu = p.epi_relu;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {

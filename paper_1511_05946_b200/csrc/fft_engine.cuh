@@ -404,17 +404,10 @@ __device__ __forceinline__ void xchg(Xbuf<G>& xb, const GroupSync<G>& gs, WF&& w
       rf(GetComp{xb.cur(), c});
     }
   } else {
-#if defined(ACDC_EXP_NOXCHG)  // timing experiment only (wrong results): no exchange at all
-    return;
-#endif
-#if !defined(ACDC_EXP_NOBAR)  // timing experiment only (races): no group barriers
     if constexpr (G::NBUF == 1) gs.sync();
-#endif
     float2* b = reinterpret_cast<float2*>(xb.cur());
     wf(PutFull{b});
-#if !defined(ACDC_EXP_NOBAR)
     gs.sync();
-#endif
     rf(GetFull{b});
     xb.flip();
   }
