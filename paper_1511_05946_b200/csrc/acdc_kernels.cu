@@ -158,6 +158,7 @@ __host__ __device__ constexpr int fwd_pstash_bytes() {
 template <int LOGN, bool H2C>
 __global__ void ACDC_LB(GeoFwd<LOGN>) acdc_fwd_kernel(KParams p) {
   using G = GeoFwd<LOGN>;
+  pdl_launch_dependents();  // the backward may stage its prologue while this grid drains
   constexpr int E = G::E;
   constexpr int PL = G::NPASS - 1;
   extern __shared__ __align__(16) float smem_f[];
@@ -685,6 +686,7 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
     if (hb) bulk_g2s(stg + G::N, p.dy + (2 * r + 1) * p.ldy, rowb, bar);
   };
   uint32_t parity = 0;
+  pdl_wait();  // everything below may read the previous kernel's output (h2 cache; dy may be y)
   if (staged && t == 0 && c.gid < npairs) issue_dy(c.gid);
   for (int64_t rp = c.gid; rp < npairs; rp += c.gstride) {
     const int64_t ra = 2 * rp;
@@ -1152,6 +1154,9 @@ static LaunchInfo info_for(int kind) {
         li.fn = (const void*)acdc_bwd_tm_kernel<LOGN>;
         geom<GeoBwdTm<LOGN>>(li, 0);
         li.red_per_cta = 1;  // the CTA's groups are pre-reduced in shared memory
+#ifndef ACDC_NO_PDL
+        li.pdl = true;  // prologue overlaps the forward's tail (pdl_wait before the h2 reads)
+#endif
         li.smem += bwd_tm_stash_bytes<LOGN>();
         li.max_per_sm = 512 / bwd_tm_cols<LOGN>();  // resident CTAs must not wait for TMEM columns
         break;

@@ -37,6 +37,12 @@ __device__ __forceinline__ float2 ld_plain_f2(const float* p) {
   return r;
 }
 
+// Programmatic dependent launch: let the next kernel in the stream start its
+// prologue now / wait here until the previous kernel's results are visible.
+// Both are no-ops without a programmatic dependency.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 template <class G>
 struct GroupCtx {
   int grp, t;

@@ -157,7 +157,22 @@ int grid_for(const LaunchInfo& li, int64_t units, int64_t* grid) {
 
 int launch(const LaunchInfo& li, int64_t grid, void* params, cudaStream_t st) {
   void* args[] = {params};
-  cudaError_t e = cudaLaunchKernel(li.fn, dim3((unsigned)grid), dim3(li.cta), args, li.smem, st);
+  cudaError_t e;
+  if (li.pdl) {  // the kernel waits (griddepcontrol.wait) before reading the previous kernel's results
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(li.cta);
+    cfg.dynamicSmemBytes = li.smem;
+    cfg.stream = st;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelExC(&cfg, li.fn, args);
+  } else {
+    e = cudaLaunchKernel(li.fn, dim3((unsigned)grid), dim3(li.cta), args, li.smem, st);
+  }
   if (e != cudaSuccess) return set_cuda_error(e);
   return ACDC_OK;
 }

@@ -34,6 +34,7 @@ struct LaunchInfo {
   int smem = 0;     // dynamic shared memory bytes
   int max_per_sm = 0;  // cap on resident CTAs per SM (TMEM columns), 0 = occupancy only
   int red_per_cta = 0;  // gradient partials one CTA writes (0: one per group)
+  bool pdl = false;     // programmatic dependent launch: may start while the previous kernel drains
 };
 
 // Persistent grid: min(CTAs needed for `units` row groups, resident CTAs).

@@ -270,3 +270,29 @@ def test_host_pipeline_matches_device_path(chunks, nbuf, ramp, direct):
     torch.testing.assert_close(dxh, dx2.cpu(), rtol=0, atol=0)
     for u, v in zip(g, g2):
         torch.testing.assert_close(u, v, rtol=1e-5, atol=1e-4)
+
+
+@pytest.mark.parametrize("n,rows", [(1024, 4096), (4096, 8192)])
+def test_backward_of_forward_output_back_to_back(n, rows):
+    """backward(dy = y) launched right after the forward that writes y: the
+    backward starts early under programmatic dependent launch and must not read
+    y (or the h2 cache) before the forward has finished."""
+    from paper_1511_05946_b200 import functional as F
+
+    rng = np.random.default_rng(n)
+    x = f32(rng, rows, n)
+    a, d, b = f32(rng, n, mean=1.0, std=0.2), f32(rng, n, mean=1.0, std=0.2), f32(rng, n, std=0.2)
+    xt, at, dt, bt = t32(x), t32(a), t32(d), t32(b)
+    hc = F.new_h2cache(rows, n, DEV)
+    g = [torch.zeros(n, device=DEV) for _ in range(3)]
+    for _ in range(3):  # repeated: the race, if any, would show on some launch
+        y = F.acdc_forward(xt, at, dt, bt, h2cache=hc)
+        dx = F.acdc_backward(xt, y, at, dt, *g, accumulate=False, h2cache=hc)
+    torch.cuda.synchronize()
+    X, A, D, B = (v.astype(np.float64) for v in (x, a, d, b))
+    yr, h2 = O.acdc_forward(X, A, D, B)
+    dxr, gar, gdr, gbr = O.acdc_backward(X, h2, y.double().cpu().numpy(), A, D)
+    assert_close_rows(y, yr, n, "y")
+    assert_close_rows(dx, dxr, n, "dx")
+    for mine, ref, nm in zip(g, (gar, gdr, gbr), ("grad_a", "grad_d", "grad_bias")):
+        assert_close_grad(mine, ref, n, rows, nm)
