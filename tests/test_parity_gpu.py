@@ -272,7 +272,7 @@ def test_host_pipeline_matches_device_path(chunks, nbuf, ramp, direct):
         torch.testing.assert_close(u, v, rtol=1e-5, atol=1e-4)
 
 
-@pytest.mark.parametrize("n,rows", [(1024, 4096), (4096, 8192)])
+@pytest.mark.parametrize("n,rows", [(1024, 4096), (4096, 2048)])
 def test_backward_of_forward_output_back_to_back(n, rows):
     """backward(dy = y) launched right after the forward that writes y: the
     backward starts early under programmatic dependent launch and must not read
@@ -293,6 +293,35 @@ def test_backward_of_forward_output_back_to_back(n, rows):
     yr, h2 = O.acdc_forward(X, A, D, B)
     dxr, gar, gdr, gbr = O.acdc_backward(X, h2, y.double().cpu().numpy(), A, D)
     assert_close_rows(y, yr, n, "y")
+    assert_close_rows(dx, dxr, n, "dx")
+    for mine, ref, nm in zip(g, (gar, gdr, gbr), ("grad_a", "grad_d", "grad_bias")):
+        assert_close_grad(mine, ref, n, rows, nm)
+
+
+@pytest.mark.parametrize("pad", [2, 4])
+def test_cached_backward_strided_dy(pad):
+    """Cached backward with dy rows at a leading dimension n + pad: pad = 4 keeps
+    16-byte row alignment (dy is bulk-copied into shared memory), pad = 2 does
+    not (dy is loaded directly)."""
+    from paper_1511_05946_b200 import functional as F
+
+    n, rows = 1024, 37
+    rng = np.random.default_rng(pad)
+    x, dy = f32(rng, rows, n), f32(rng, rows, n)
+    a, d, b = f32(rng, n, mean=1.0, std=0.2), f32(rng, n, mean=1.0, std=0.2), f32(rng, n, std=0.2)
+    wide = torch.zeros(rows, n + pad, device=DEV)
+    wide[:, :n] = t32(dy)
+    dyv = wide[:, :n]
+    assert dyv.stride(0) == n + pad
+    xt, at, dt, bt = t32(x), t32(a), t32(d), t32(b)
+    hc = F.new_h2cache(rows, n, DEV)
+    F.acdc_forward(xt, at, dt, bt, h2cache=hc)
+    g = [torch.zeros(n, device=DEV) for _ in range(3)]
+    dx = F.acdc_backward(xt, dyv, at, dt, *g, accumulate=False, h2cache=hc)
+    torch.cuda.synchronize()
+    X, A, D, B, DY = (v.astype(np.float64) for v in (x, a, d, b, dy))
+    _, h2 = O.acdc_forward(X, A, D, B)
+    dxr, gar, gdr, gbr = O.acdc_backward(X, h2, DY, A, D)
     assert_close_rows(dx, dxr, n, "dx")
     for mine, ref, nm in zip(g, (gar, gdr, gbr), ("grad_a", "grad_d", "grad_bias")):
         assert_close_grad(mine, ref, n, rows, nm)
