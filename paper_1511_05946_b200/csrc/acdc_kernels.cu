@@ -280,6 +280,35 @@ __global__ void ACDC_LB(GeoFwd<LOGN>) acdc_fwd_kernel(KParams p) {
 template <int LOGN, bool H2C = false>
 using GeoBwd = Geo<LOGN, (H2C ? 1 : 3) * Geo<LOGN>::E, (H2C ? fp_gpc<LOGN, ACDC_BWD_CTA>() : 0)>;
 
+// Gradient partials of the CTA's groups pre-reduced on chip (small n: up to 64
+// groups per CTA, whose per-group partials would outweigh the rows): every
+// group writes its 3N partials into its own exchange buffers once its rows are
+// done (exchange buffers and stash: the stash is read into registers and the
+// group synchronised first), then the CTA adds them in group order (fp64) and
+// writes one partial.
+template <class G>
+__host__ __device__ constexpr bool cta_red() {
+  return G::GPC > 1 && G::STASH_SMEM && G::GROUP_FLOATS >= 3 * G::N && !G::SPLIT;
+}
+template <class G>
+__device__ __forceinline__ float* part_dst(const KParams& p, const GroupCtx<G>& c, float* smem_f) {
+  if constexpr (cta_red<G>()) return smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS;
+  else return p.ws + c.gid * 3 * G::N;
+}
+template <class G>
+__device__ __forceinline__ void finish_partials(const KParams& p, const float* smem_f) {
+  if constexpr (cta_red<G>()) {
+    __syncthreads();
+    float* out = p.ws + (int64_t)blockIdx.x * 3 * G::N;
+    for (int i = threadIdx.x; i < 3 * G::N; i += blockDim.x) {
+      double acc = 0.0;
+#pragma unroll 4
+      for (int g = 0; g < G::GPC; ++g) acc += (double)smem_f[G::TAB_FLOATS + g * G::GROUP_FLOATS + i];
+      out[i] = (float)acc;
+    }
+  }
+}
+
 // Backward parameter stash (fast-pairing path): d at every thread's 8 spectral
 // slots, [slot][t] float2 (d_lo, d_hi), shared by the CTA's groups and filled
 // once per launch.  The slot pass then has no global parameter loads, so the
@@ -486,12 +515,15 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
       }
     }
     // per-group partials
-    float* w = p.ws + c.gid * 3 * G::N;
+    float2 gav[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) gav[q] = st_ga2[q * T];
+    if constexpr (cta_red<G>()) gs.sync();  // the group's stash is read before its region is reused
+    float* w = part_dst<G>(p, c, smem_f);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const float2 g = st_ga2[q * T];
-      w[2 * (fm.jsp + q * S)] = g.x;
-      w[2 * (fm.jsp + q * S) + 1] = g.y;
+      w[2 * (fm.jsp + q * S)] = gav[q].x;
+      w[2 * (fm.jsp + q * S) + 1] = gav[q].y;
     }
 #pragma unroll
     for (int s = 0; s < 8; ++s) {
@@ -500,6 +532,7 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
       *fm.plo(w + 2 * G::N, s) = acc_b[2 * s];
       *fm.phi(w + 2 * G::N, s) = acc_b[2 * s + 1];
     }
+    finish_partials<G>(p, smem_f);
     return;
   }
 
@@ -573,12 +606,16 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
       }
   }
   // per-group partials: ws[gid][0] = grad_a, [1] = grad_d, [2] = grad_bias
-  float* w = p.ws + c.gid * 3 * G::N;
+  float gar[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) gar[i] = st_ga[i * T];
+  if constexpr (cta_red<G>()) gs.sync();  // the group's stash is read before its region is reused
+  float* w = part_dst<G>(p, c, smem_f);
   const RowPtrW<G> wa(w, t);
 #pragma unroll
   for (int b = 0; b < E / RL; ++b)
 #pragma unroll
-    for (int q = 0; q < RL; ++q) *wa.template at<PL>(b, q) = st_ga[(b * RL + q) * T];
+    for (int q = 0; q < RL; ++q) *wa.template at<PL>(b, q) = gar[b * RL + q];
 #pragma unroll
   for (int i = 0; i < E / 2; ++i) {
     *sl.plo(w + G::N, i) = acc_d[2 * i];
@@ -586,6 +623,7 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
     *sl.plo(w + 2 * G::N, i) = acc_b[2 * i];
     *sl.phi(w + 2 * G::N, i) = acc_b[2 * i + 1];
   }
+  finish_partials<G>(p, smem_f);
 }
 
 // Cached-h2 backward with its per-thread gradient accumulators in TMEM
@@ -1134,6 +1172,7 @@ static LaunchInfo info_for(int kind) {
       li.fn = (const void*)acdc_bwd_kernel<LOGN, false>;
       geom<GB>(li, GB::GSCRATCH_FLOATS);
       li.smem += bwd_dstash_bytes<LOGN, false>();
+      if (cta_red<GB>()) li.red_per_cta = 1;
       break;
     case K_DCT2:
       li.fn = (const void*)acdc_dct2_kernel<LOGN>;
@@ -1165,6 +1204,7 @@ static LaunchInfo info_for(int kind) {
       li.fn = FP ? (const void*)acdc_bwd_kernel<LOGN, FP> : nullptr;
       geom<GBC>(li, GBC::GSCRATCH_FLOATS);
       li.smem += bwd_dstash_bytes<LOGN, FP>();
+      if (cta_red<GBC>()) li.red_per_cta = 1;
       break;
   }
   return li;
