@@ -1,5 +1,5 @@
 """Forward / backward parity of the loaded library at one size vs the fp64 oracle
-(for single-size A/B builds: ACDC_LIB_PATH=variant.so python scripts/fwd_check.py N rows)."""
+(test tooling for single-size A/B builds: ACDC_LIB_PATH=variant.so python tests/variant_check.py N rows)."""
 import os
 import sys
 
