@@ -17,7 +17,7 @@
 #include <cstdint>
 #include <cstdio>
 
-#include "fft_engine.cuh"
+#include "kernel_common.cuh"  // fft_engine.cuh, pdl_*
 #include "runtime.h"
 #include "tmem.cuh"
 
@@ -161,6 +161,7 @@ __host__ __device__ constexpr int afdf_tmf_smem() {
 template <int LOGN>
 __global__ void ACDC_LB(GeoFT<LOGN>) afdf_fwd_tm_kernel(FParams p) {
   using G = GeoFT<LOGN>;
+  pdl_launch_dependents();  // the backward may stage its prologue while this grid drains
   constexpr int T = G::T;
   static_assert(afdf_tm_ok<LOGN>(), "TMEM AFDF plan");
   extern __shared__ __align__(16) float smem_f[];
@@ -387,6 +388,7 @@ __global__ void ACDC_LB(GeoFT<LOGN>) afdf_bwd_tm_kernel(FParams p) {
 #pragma unroll
     for (int k = 4; k < 8; ++k) tmem_st16(ta + 16 * k, z);
   }
+  pdl_wait();  // x and dy (which may be the forward's y) are read from here on
   const float scale = 1.0f / G::N;
   for (int64_t r = gid; r < p.rows; r += gstride) {
     const float2* xr = p.x + r * p.ldx + t;
@@ -537,6 +539,9 @@ static LaunchInfo finfo(int kind) {
       li.scratch = 0;
       li.smem = afdf_tm_smem<LOGN>();
       li.max_per_sm = 1;  // 512 TMEM columns per CTA
+#ifndef ACDC_NO_PDL
+      li.pdl = true;  // prologue overlaps the forward's tail
+#endif
     }
   }
 #endif
