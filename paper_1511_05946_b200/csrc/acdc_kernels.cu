@@ -325,6 +325,7 @@ __host__ __device__ constexpr int bwd_dstash_bytes() {
 template <int LOGN, bool H2C>
 __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
   using G = GeoBwd<LOGN, H2C>;
+  pdl_launch_dependents();  // the reduction may launch early; it waits for this grid
   constexpr int E = G::E;
   constexpr int T = G::T;
   constexpr int PL = G::NPASS - 1;
@@ -351,6 +352,7 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
   }
   const float2 *tw, *cp;
   stage_tables<G>(p.tab, smem_f, tw, cp);
+  pdl_wait();  // x, dy (maybe the forward's y) and the h2 cache are read from here on
   // fast-pairing path: grad_a partials as float2 [q][T] (positions 2m, 2m+1)
   float2* st_ga2 = reinterpret_cast<float2*>(sbase + (H2C ? 0 : 2 * E * T)) + t;
   float acc_d[E], acc_b[E];
@@ -669,6 +671,7 @@ __host__ __device__ constexpr int bwd_tm_cols() {
 template <int LOGN>
 __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
   using G = GeoBwdTm<LOGN>;
+  pdl_launch_dependents();  // the reduction may launch early; it waits for this grid
   constexpr int T = G::T;
   constexpr int S = FastMap<G>::S;
   constexpr int COLS = bwd_tm_cols<LOGN>();
@@ -1036,6 +1039,7 @@ template <bool SGD>
 __global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __restrict__ ws, int64_t groups, int n,
                                                                float* ga, float* gd, float* gb, int accumulate,
                                                                SgdDev sgd) {
+  pdl_wait();  // the backward's partials
   __shared__ double part[8][33];
   const int o = threadIdx.x & 31, s = threadIdx.x >> 5;
   const int64_t total = 3LL * n;
@@ -1091,6 +1095,7 @@ __global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __re
 constexpr int RED_CHUNK = 160;
 __global__ void __launch_bounds__(256) acdc_grad_partial_kernel(const float* __restrict__ ws, int64_t groups,
                                                                 int64_t total, double* __restrict__ tmp) {
+  pdl_wait();  // the backward's partials
   __shared__ double part[8][33];
   const int o = threadIdx.x & 31, s = threadIdx.x >> 5;
   const int64_t idx = blockIdx.x * 32LL + o;
@@ -1136,6 +1141,26 @@ __global__ void __launch_bounds__(256) acdc_grad_final_kernel(const double* __re
   }
 }
 
+// 256-thread reduction launch that may start while the backward drains
+// (programmatic dependent launch; the kernel waits before reading).
+template <class... KA, class... A>
+static void launch_pdl(void (*kern)(KA...), dim3 grid, cudaStream_t st, A... args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr.val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.stream = st;
+  cfg.attrs = &attr;
+#ifdef ACDC_NO_PDL
+  cfg.numAttrs = 0;
+#else
+  cfg.numAttrs = 1;
+#endif
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // fp64 chunk-partial bytes the two-stage reduction needs after the partials.
 static size_t red_tmp_bytes(int64_t groups, int32_t n) {
   if (groups <= RED_CHUNK) return 0;
@@ -1171,6 +1196,9 @@ static LaunchInfo info_for(int kind) {
     case K_BWD:
       li.fn = (const void*)acdc_bwd_kernel<LOGN, false>;
       geom<GB>(li, GB::GSCRATCH_FLOATS);
+#ifndef ACDC_NO_PDL
+      li.pdl = true;
+#endif
       li.smem += bwd_dstash_bytes<LOGN, false>();
       if (cta_red<GB>()) li.red_per_cta = 1;
       break;
@@ -1203,6 +1231,9 @@ static LaunchInfo info_for(int kind) {
 #endif
       li.fn = FP ? (const void*)acdc_bwd_kernel<LOGN, FP> : nullptr;
       geom<GBC>(li, GBC::GSCRATCH_FLOATS);
+#ifndef ACDC_NO_PDL
+      li.pdl = true;
+#endif
       li.smem += bwd_dstash_bytes<LOGN, FP>();
       if (cta_red<GBC>()) li.red_per_cta = 1;
       break;
@@ -1439,7 +1470,7 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
     size_t off = (size_t)groups * (3 * (size_t)n + (size_t)scratch_floats) * sizeof(float);
     off = (off + 7) & ~(size_t)7;
     double* tmp = reinterpret_cast<double*>(static_cast<char*>(ws) + off);
-    acdc_grad_partial_kernel<<<dim3(blocks, chunks), 256, 0, st>>>((const float*)ws, groups, total, tmp);
+    launch_pdl(acdc_grad_partial_kernel, dim3(blocks, chunks), st, (const float*)ws, groups, total, tmp);
     const int fb = (int)((total + 255) / 256);
     if (sgd)
       acdc_grad_final_kernel<true><<<fb, 256, 0, st>>>(tmp, chunks, n, grad_a, grad_d, grad_bias, accumulate, *sgd);
@@ -1450,11 +1481,11 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
     return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
   }
   if (sgd)
-    acdc_grad_reduce_kernel<true><<<blocks, 256, 0, st>>>((const float*)ws, groups, n, grad_a, grad_d, grad_bias,
-                                                          accumulate, *sgd);
+    launch_pdl(acdc_grad_reduce_kernel<true>, dim3(blocks), st, (const float*)ws, groups, n, grad_a, grad_d,
+               grad_bias, accumulate, *sgd);
   else
-    acdc_grad_reduce_kernel<false><<<blocks, 256, 0, st>>>((const float*)ws, groups, n, grad_a, grad_d, grad_bias,
-                                                           accumulate, SgdDev{});
+    launch_pdl(acdc_grad_reduce_kernel<false>, dim3(blocks), st, (const float*)ws, groups, n, grad_a, grad_d,
+               grad_bias, accumulate, SgdDev{});
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
 }
