@@ -1039,7 +1039,8 @@ template <bool SGD>
 __global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __restrict__ ws, int64_t groups, int n,
                                                                float* ga, float* gd, float* gb, int accumulate,
                                                                SgdDev sgd) {
-  pdl_wait();  // the backward's partials
+  pdl_launch_dependents();  // e.g. the next cascade block's backward: its prologue overlaps this
+  pdl_wait();               // the backward's partials
   __shared__ double part[8][33];
   const int o = threadIdx.x & 31, s = threadIdx.x >> 5;
   const int64_t total = 3LL * n;
