@@ -39,6 +39,7 @@ template <int LOGN>
 __global__ void ACDC_LB(Geo<LOGN>) cascade_fwd_kernel(CParams p) {
   using G = Geo<LOGN>;
   static_assert(G::FP, "cascade fusion needs the fast-pairing path");
+  pdl_launch_dependents();  // the last block's backward may stage its prologue while this grid drains
   constexpr int N = G::N, T = G::T, S = FastMap<G>::S;
   extern __shared__ __align__(16) float smem_f[];
   const auto c = group_ctx<G>();
