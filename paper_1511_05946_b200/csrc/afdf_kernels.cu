@@ -390,12 +390,16 @@ __global__ void ACDC_LB(GeoFT<LOGN>) afdf_bwd_tm_kernel(FParams p) {
   }
   pdl_wait();  // x and dy (which may be the forward's y) are read from here on
   const float scale = 1.0f / G::N;
+  float2 xn[16];  // this row's x, loaded during the previous row's last transform
+  if (gid < p.rows) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) xn[q] = __ldg(p.x + gid * p.ldx + t + q * T);
+  }
   for (int64_t r = gid; r < p.rows; r += gstride) {
-    const float2* xr = p.x + r * p.ldx + t;
     const float2* dyr = p.dy + r * p.ldy + t;
     float2 v[16], g[16];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) v[q] = __ldg(xr + q * T);
+    for (int q = 0; q < 16; ++q) v[q] = xn[q];
 #pragma unroll
     for (int q = 0; q < 16; ++q) g[q] = __ldg(dyr + q * T);  // in flight across the h2 transform
     {
@@ -435,6 +439,10 @@ __global__ void ACDC_LB(GeoFT<LOGN>) afdf_bwd_tm_kernel(FParams p) {
         v[q] = cmul(conjf2(v[q]), ld_param(p.d + t + q * T));
       }
       tmem_st16(ta + 96 + 16 * half, ad);
+    }
+    if (r + gstride < p.rows) {  // the next row's x: in flight across the last transform
+#pragma unroll
+      for (int q = 0; q < 16; ++q) xn[q] = __ldg(p.x + (r + gstride) * p.ldx + t + q * T);
     }
     fft_passes<G>(v, xb, gs, tw, t);  // g1 = conj(FFT(V)) / N  (times N: the 1/N cancels, see header)
     float2* oxr = p.y + r * p.ldo + t;
