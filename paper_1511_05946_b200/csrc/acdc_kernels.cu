@@ -204,7 +204,11 @@ __global__ void ACDC_LB(GeoFwd<LOGN>) acdc_fwd_kernel(KParams p) {
           dct2_post(v[s], w[s], cs, fm.special(s), chi, xl, xh);
           if constexpr (H2C) {
             float4* hc = reinterpret_cast<float4*>(p.h2c + rp * 2 * G::N) + t;  // [slot s][t]
+#ifdef ACDC_H2_KEEP  // normal caching: the tail of the cache stays in L2 for a last-first backward
+            hc[s * G::T] = make_float4(xl.x, xl.y, xh.x, xh.y);
+#else
             __stcs(hc + s * G::T, make_float4(xl.x, xl.y, xh.x, xh.y));
+#endif
           }
           float dl, dh, bl, bh;
           if constexpr (PST) {
@@ -637,6 +641,9 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
 #ifndef ACDC_BWD_TM_CTA
 #define ACDC_BWD_TM_CTA 512
 #endif
+#ifndef ACDC_BWD_REV  // 1: the TMEM backward visits row pairs last-first (L2 reuse of the forward's tail)
+#define ACDC_BWD_REV 1
+#endif
 #ifndef ACDC_TM_MAX_LOGN  // largest size with tables in smem (n = 16384 keeps them in global memory)
 #define ACDC_TM_MAX_LOGN 13
 #endif
@@ -727,14 +734,18 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
     if (hb) bulk_g2s(stg + G::N, p.dy + (2 * r + 1) * p.ldy, rowb, bar);
   };
   uint32_t parity = 0;
+  // Row pairs are visited last-first: the forward just wrote / read the last
+  // row pairs' h2 cache and x, which are then still in L2.
+  auto rmap = [&](int64_t i) { return ACDC_BWD_REV ? npairs - 1 - i : i; };
   pdl_wait();  // everything below may read the previous kernel's output (h2 cache; dy may be y)
-  if (staged && t == 0 && c.gid < npairs) issue_dy(c.gid);
-  for (int64_t rp = c.gid; rp < npairs; rp += c.gstride) {
+  if (staged && t == 0 && c.gid < npairs) issue_dy(rmap(c.gid));
+  for (int64_t it = c.gid; it < npairs; it += c.gstride) {
+    const int64_t rp = rmap(it);
     const int64_t ra = 2 * rp;
     const bool hasb = ra + 1 < p.rows;
     const int64_t rb = hasb ? ra + 1 : ra;
-    if (t == 0 && rp + ACDC_PF_DIST * c.gstride < npairs) {  // a later row pair -> L2
-      const int64_t nr = 2 * (rp + ACDC_PF_DIST * c.gstride);
+    if (t == 0 && it + ACDC_PF_DIST * c.gstride < npairs) {  // a later row pair -> L2
+      const int64_t nr = 2 * rmap(it + ACDC_PF_DIST * c.gstride);
       prefetch_row_l2(p.dy + nr * p.ldy, G::N);
       prefetch_row_l2(p.x + nr * p.ldx, G::N);
       if (nr + 1 < p.rows) {
@@ -804,7 +815,7 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
     }
     fft_passes<G, 0>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
     // exchange 4 has passed: buffer A (last read at exchange 3) takes the next dy
-    if (staged && t == 0 && rp + c.gstride < npairs) issue_dy(rp + c.gstride);
+    if (staged && t == 0 && it + c.gstride < npairs) issue_dy(rmap(it + c.gstride));
     float2 ga[8], gb[8];
     fp_out_pairs<G>(v, ga, gb, fm);
     {
