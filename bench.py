@@ -418,7 +418,7 @@ def e2e_measure(F, n, B, a, d, bias, dev, world, steps, h2cache=None):
     dxh = torch.empty(B, n).pin_memory()
     gh = torch.empty(3, n).pin_memory()
     grads = torch.zeros(3, n, device=dev)
-    pipe = F.HostPipeline(n, B, dev, chunks=8, h2cache=h2cache is not None)
+    pipe = F.HostPipeline(n, B, dev, chunks=4, h2cache=h2cache is not None)  # scripts/e2e_sweep.py
 
     def step():
         pipe.step(xh, dyh, yh, dxh, a, d, bias, (grads[0], grads[1], grads[2]), accumulate=False)
@@ -443,7 +443,8 @@ def e2e_measure(F, n, B, a, d, bias, dev, world, steps, h2cache=None):
         "h2d_bytes_per_step": 2 * B * n * 4,
         "d2h_bytes_per_step": 2 * B * n * 4 + 3 * n * 4,
         "steps": steps,
-        "path": "functional.HostPipeline (C ABI kernels; pinned host x, dy -> y, dx, grads; 8 chunks, 3 streams)",
+        "path": "functional.HostPipeline (C ABI kernels; pinned host x, dy -> y, dx, grads; 4 chunks, 3 streams, "
+                "uploads of a step overlap the previous step's downloads)",
     }
 
 

@@ -473,11 +473,18 @@ class HostPipeline:
     ``direct_out``: the kernels store y and dx straight into the pinned host
     buffers (mapped through unified addressing: posted PCIe writes from the
     SMs), so there is no device->host copy stage to schedule around.
+
+    ``overlap_steps``: a step's uploads wait only for their device buffers,
+    not for the caller's stream, so they overlap the previous step's last
+    downloads (the kernels still follow the caller's stream: parameters and
+    gradients).  The host inputs must not be rewritten until the step's
+    uploads have completed, as with any asynchronous copy.
     """
 
     def __init__(self, n: int, rows: int, device, chunks: int = 8, h2cache: bool = True, nbuf: int = 2,
-                 ramp: bool = False, direct_out: bool = False):
+                 ramp: bool = False, direct_out: bool = False, overlap_steps: bool = True):
         self.n, self.rows, self.dev = n, rows, torch.device(device)
+        self.overlap_steps = overlap_steps
         self.direct_out = direct_out
         self.spans = self.plan(rows, chunks, ramp)
         self.chunks = len(self.spans)
@@ -494,6 +501,10 @@ class HostPipeline:
         self.s_in = torch.cuda.Stream(self.dev)
         self.s_cmp = torch.cuda.Stream(self.dev)
         self.s_out = torch.cuda.Stream(self.dev)
+        # last compute / download that used each buffer set, across steps: the next
+        # step's uploads only wait for these, so they overlap this step's downloads
+        self._buf_done = [None] * self.nbuf
+        self._buf_down = [None] * self.nbuf
         prepare(n, self.dev)
 
     @staticmethod
@@ -533,30 +544,35 @@ class HostPipeline:
         """All host tensors must be pinned CPU fp32 (rows, n).  Returns after
         enqueueing; call ``torch.cuda.synchronize()`` (or an event) to wait."""
         ga, gd, gb = grads
+        up = [torch.cuda.Event(enable_timing=timeline) for _ in self.spans]
+        done = [torch.cuda.Event(enable_timing=timeline) for _ in self.spans]
+        down = [torch.cuda.Event(enable_timing=timeline) for _ in self.spans]
+        cur = torch.cuda.current_stream(self.dev)
+        # the kernels and downloads follow the caller's stream (parameters, gradients);
+        # the uploads only need their buffer set free (previous step included)
+        for s in (self.s_cmp, self.s_out) if self.overlap_steps else (self.s_in, self.s_cmp, self.s_out):
+            s.wait_stream(cur)
         if not accumulate:
             with torch.cuda.stream(self.s_cmp):
                 ga.zero_()
                 gd.zero_()
                 gb.zero_()
-        up = [torch.cuda.Event(enable_timing=timeline) for _ in self.spans]
-        done = [torch.cuda.Event(enable_timing=timeline) for _ in self.spans]
-        down = [torch.cuda.Event(enable_timing=timeline) for _ in self.spans]
-        cur = torch.cuda.current_stream(self.dev)
-        for s in (self.s_in, self.s_cmp, self.s_out):
-            s.wait_stream(cur)
         nb = self.nbuf
         for i, (lo, hi) in enumerate(self.spans):
             k, m = i % nb, hi - lo
             with torch.cuda.stream(self.s_in):
-                if i >= nb:  # buffer set k is free once chunk i-nb was computed
-                    self.s_in.wait_event(done[i - nb])
+                prev = done[i - nb] if i >= nb else self._buf_done[k]
+                if prev is not None:  # buffer set k is free once its previous chunk was computed
+                    self.s_in.wait_event(prev)
                 self.xd[k][:m].copy_(x_host[lo:hi], non_blocking=True)
                 self.dyd[k][:m].copy_(dy_host[lo:hi], non_blocking=True)
                 up[i].record(self.s_in)
             with torch.cuda.stream(self.s_cmp):
                 self.s_cmp.wait_event(up[i])
-                if i >= nb and not self.direct_out:  # outputs of chunk i-nb must be downloaded first
-                    self.s_cmp.wait_event(down[i - nb])
+                if not self.direct_out:  # outputs of the buffer's previous chunk must be downloaded first
+                    prev = down[i - nb] if i >= nb else self._buf_down[k]
+                    if prev is not None:
+                        self.s_cmp.wait_event(prev)
                 hc = self.hc[k] if self.hc is not None else None
                 yo = y_host[lo:hi] if self.direct_out else self.yd[k][:m]
                 dxo = dx_host[lo:hi] if self.direct_out else self.dxd[k][:m]
@@ -572,6 +588,9 @@ class HostPipeline:
                 y_host[lo:hi].copy_(self.yd[k][:m], non_blocking=True)
                 dx_host[lo:hi].copy_(self.dxd[k][:m], non_blocking=True)
                 down[i].record(self.s_out)
+        for i in range(max(0, len(self.spans) - nb), len(self.spans)):
+            self._buf_done[i % nb] = done[i]
+            self._buf_down[i % nb] = down[i]
         for s in (self.s_in, self.s_cmp, self.s_out):
             cur.wait_stream(s)
         if timeline:  # (upload, compute, download) completion events per chunk
