@@ -17,9 +17,10 @@ yh, dxh = torch.empty(B, n).pin_memory(), torch.empty(B, n).pin_memory()
 gh = torch.empty(3, n).pin_memory()
 a, d, b = (torch.randn(n, device=dev) for _ in range(3))
 grads = torch.zeros(3, n, device=dev)
-for chunks, nbuf, ov in [(4, 2, True), (2, 2, True), (3, 2, True), (6, 2, True), (4, 3, True), (8, 2, True)]:
+for chunks, nbuf, ov, direct in [(4, 2, True, False), (4, 2, True, True), (8, 2, True, True), (4, 2, True, False),
+                                 (4, 2, True, True)]:
     if True:
-        pipe = F.HostPipeline(n, B, dev, chunks=chunks, nbuf=nbuf, overlap_steps=ov)
+        pipe = F.HostPipeline(n, B, dev, chunks=chunks, nbuf=nbuf, overlap_steps=ov, direct_out=direct)
 
         def step():
             pipe.step(xh, dyh, yh, dxh, a, d, b, (grads[0], grads[1], grads[2]), accumulate=False)
@@ -33,5 +34,5 @@ for chunks, nbuf, ov in [(4, 2, True), (2, 2, True), (3, 2, True), (6, 2, True),
             step()
         e1.record()
         torch.cuda.synchronize()
-        print(f"chunks={chunks} nbuf={nbuf} overlap={ov} rows/s={B * steps / (e0.elapsed_time(e1) / 1e3):.4g}",
+        print(f"chunks={chunks} nbuf={nbuf} overlap={ov} direct={direct} rows/s={B * steps / (e0.elapsed_time(e1) / 1e3):.4g}",
               flush=True)
