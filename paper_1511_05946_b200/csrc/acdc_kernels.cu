@@ -644,6 +644,9 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
 #ifndef ACDC_BWD_REV  // 1: the TMEM backward visits row pairs last-first (L2 reuse of the forward's tail)
 #define ACDC_BWD_REV 1
 #endif
+#ifndef ACDC_TM_GTAB  // 1: also build the TMEM backward where the tables stay in global memory
+#define ACDC_TM_GTAB 0
+#endif
 #ifndef ACDC_TM_MAX_LOGN  // largest size with tables in smem (n = 16384 keeps them in global memory)
 #define ACDC_TM_MAX_LOGN 13
 #endif
@@ -665,7 +668,7 @@ __host__ __device__ constexpr bool bwd_tm_ok() {
   using G = GeoBwdTm<LOGN>;
   // groups must be whole warps: the TMEM accesses are warp-collective and the
   // groups of one warp could run different row counts
-  return G::FP && G::TW_SMEM && !G::SPLIT && G::T >= 32 && LOGN <= ACDC_TM_MAX_LOGN &&
+  return G::FP && (G::TW_SMEM || ACDC_TM_GTAB) && !G::SPLIT && G::T >= 32 && LOGN <= ACDC_TM_MAX_LOGN &&
          G::SMEM_BYTES + bwd_tm_stash_bytes<LOGN>() <= G::SMEM_LIMIT && (G::CTA / 32 / 4) * 48 <= 512;
 }
 template <int LOGN>
@@ -696,7 +699,8 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
   // passed, and read from there at the top of the next iteration.
   float* stg = smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS;
   uint64_t* bar = &dy_bar[c.grp];
-  const bool staged = p.stage != 0;
+  // (one exchange buffer: the next dy cannot land while exchange 4 is read)
+  const bool staged = G::NBUF == 2 && p.stage != 0;
   if (staged && t == 0) mbar_init(bar, 1);
   float2* dst_all = reinterpret_cast<float2*>(smem_f + G::SMEM_BYTES / 4);
   const float2* dst = dst_all + t;          // [s][t] (d_lo, d_hi)
@@ -713,6 +717,7 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
   tmem_fence_before();
   const float2 *tw, *cp;
   stage_tables<G>(p.tab, smem_f, tw, cp);  // __syncthreads: stashes and the TMEM base are published
+  if constexpr (!G::TW_SMEM) __syncthreads();  // (tables in global memory: no barrier in stage_tables)
   tmem_fence_after();
   // columns of this thread: [0,16) grad_bias bins, [16,32) grad_d bins, [32,48) grad_a positions
   const uint32_t ta = tmem_addr(tm_slot, warp, (warp >> 2) * 48);

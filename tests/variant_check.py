@@ -24,7 +24,11 @@ yr, h2 = O.acdc_forward(X, A, D, B)
 dxr, gar, gdr, gbr = O.acdc_backward(X, h2, DY, A, D)
 for mode in ("recompute", "h2cache"):
     hc = F.new_h2cache(rows, n, dev) if mode == "h2cache" else None
-    y = F.acdc_forward(t(x), t(a), t(d), t(b), h2cache=hc)
+    try:
+        y = F.acdc_forward(t(x), t(a), t(d), t(b), h2cache=hc)
+    except ValueError as e:  # mode not supported by this variant
+        print(mode, "skipped:", e)
+        continue
     g = [torch.zeros(n, device=dev) for _ in range(3)]
     dx = F.acdc_backward(t(x), t(dy), t(a), t(d), *g, accumulate=False, h2cache=hc)
     torch.cuda.synchronize()
