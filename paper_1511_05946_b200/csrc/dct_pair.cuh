@@ -49,7 +49,7 @@ struct Slots {
   __device__ __forceinline__ int xlo(int i) const { return padi(t) + padoff(i * T); }
   __device__ __forceinline__ int xhi(int i) const {
     if constexpr (T % 16 == 0) {
-      const int hb = t + ((t + 15) >> 4);
+      const int hb = t + ACDC_PADS * ((t + 15) >> 4);
       return (i == 0 && t0) ? padoff(N / 2) : padoff(N - i * T) - hb;
     } else {
       return padi(hi(i));

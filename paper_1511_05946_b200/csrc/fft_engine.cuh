@@ -257,6 +257,9 @@ struct Plan {
 // hold GPC row-pair groups (512 threads when T <= 512) sharing one copy of the
 // tables; the plan prefers tables in smem and double-buffered exchanges and
 // falls back (single buffer, tables in global) until the CTA fits in 227 KB.
+#ifndef ACDC_PADS  // float2 padding slots per 16 in the exchange buffers
+#define ACDC_PADS 1
+#endif
 #ifndef ACDC_E32_FROM  // log2 N from which each thread holds 32 values (T = N / 32)
 #define ACDC_E32_FROM 15
 #endif
@@ -268,7 +271,7 @@ struct Geo : Plan<LOGN> {
   static constexpr int T = N / E;                                 // threads per row-pair group
   static constexpr int GPC = GPCX ? GPCX : (T <= 512 ? 512 / T : 1);  // groups per CTA
   static constexpr int CTA = T * GPC;                             // threads per CTA
-  static constexpr int PADN = N + N / 16;                         // padded float2 slots per buffer
+  static constexpr int PADN = N + ACDC_PADS * (N / 16);          // padded float2 slots per buffer
   static constexpr bool SPLIT = (N >= 32768);                     // exchange re / im separately
   static constexpr int BUF_FLOATS = SPLIT ? PADN : 2 * PADN;      // floats per exchange buffer
   static constexpr int STASH_FLOATS = STASH * T;                  // per group
@@ -300,12 +303,14 @@ struct Geo : Plan<LOGN> {
 #endif
 };
 
-// Padded exchange index (one float2 of padding per 16 slots).  For a
+// Padded exchange index (ACDC_PADS float2 of padding per 16 slots).  For a
 // power-of-two stride S and base j < S (or S, j multiples of 16):
 //   padi(j + q*S) = padi(j) + padoff(q*S)
 // which lets every exchange address be a base register plus an immediate.
-__host__ __device__ constexpr int padi(int i) { return i + (i >> 4); }
-__host__ __device__ constexpr int padoff(int off) { return off + (off >> 4); }
+// With an even pad every 16-slot run starts 16-byte aligned, so the first
+// pass (contiguous outputs per thread) stores 128-bit pairs.
+__host__ __device__ constexpr int padi(int i) { return i + ACDC_PADS * (i >> 4); }
+__host__ __device__ constexpr int padoff(int off) { return off + ACDC_PADS * (off >> 4); }
 
 // Group-local barrier: warp mask for T <= 32, named barrier otherwise.
 template <class G>
@@ -358,14 +363,20 @@ __device__ __forceinline__ float4 tab_load4(const float2* tab) {
 // Element accessors for one exchange, taking PADDED indices: full float2
 // slots, or one component at a time when the buffer holds N floats (SPLIT).
 struct PutFull {
+  static constexpr bool kPair = true;
   float2* b;
   __device__ __forceinline__ void operator()(int pi, float2 v) const { b[pi] = v; }
+  // slots pi, pi + 1 (pi even): one 128-bit store
+  __device__ __forceinline__ void pair(int pi, float2 v0, float2 v1) const {
+    *reinterpret_cast<float4*>(b + pi) = make_float4(v0.x, v0.y, v1.x, v1.y);
+  }
 };
 struct GetFull {
   const float2* b;
   __device__ __forceinline__ void operator()(int pi, float2& d) const { d = b[pi]; }
 };
 struct PutComp {
+  static constexpr bool kPair = false;
   float* b;
   int c;
   __device__ __forceinline__ void operator()(int pi, float2 v) const { b[pi] = c ? v.y : v.x; }
@@ -477,8 +488,13 @@ __device__ __forceinline__ void pass_store(const float2 (&v)[G::E], const PUT& p
     const int j = j0 + b * G::T;
     const int k = j & (NS - 1);
     const int pd = padi((j - k) * R + k);
+    if constexpr (NS == 1 && ACDC_PADS % 2 == 0 && PUT::kPair && R >= 2) {
 #pragma unroll
-    for (int q = 0; q < R; ++q) put(pd + padoff(q * NS), v[b * R + q]);
+      for (int q = 0; q < R; q += 2) put.pair(pd + q, v[b * R + q], v[b * R + q + 1]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < R; ++q) put(pd + padoff(q * NS), v[b * R + q]);
+    }
   }
 }
 
