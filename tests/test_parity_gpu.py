@@ -272,6 +272,36 @@ def test_host_pipeline_matches_device_path(chunks, nbuf, ramp, direct):
         torch.testing.assert_close(u, v, rtol=1e-5, atol=1e-4)
 
 
+@pytest.mark.parametrize("overlap", [True, False])
+def test_host_pipeline_consecutive_steps(overlap):
+    """Back-to-back HostPipeline steps with different inputs and outputs: with
+    overlap_steps a step's uploads run under the previous step's downloads, so
+    every step's y, dx and gradients must still equal its own device call."""
+    from paper_1511_05946_b200 import functional as F
+
+    n, rows, steps = 2048, 1000, 3
+    rng = np.random.default_rng(33)
+    a, d, b = (t32(f32(rng, n, mean=m, std=0.3)) for m in (1.0, 1.0, 0.0))
+    pipe = F.HostPipeline(n, rows, DEV, chunks=4, overlap_steps=overlap)
+    xs = [torch.as_tensor(f32(rng, rows, n)).pin_memory() for _ in range(steps)]
+    dys = [torch.as_tensor(f32(rng, rows, n)).pin_memory() for _ in range(steps)]
+    ys = [torch.empty(rows, n).pin_memory() for _ in range(steps)]
+    dxs = [torch.empty(rows, n).pin_memory() for _ in range(steps)]
+    gs = [[torch.zeros(n, device=DEV) for _ in range(3)] for _ in range(steps)]
+    for i in range(steps):  # no host sync between steps
+        pipe.step(xs[i], dys[i], ys[i], dxs[i], a, d, b, gs[i], accumulate=False)
+    torch.cuda.synchronize()
+    for i in range(steps):
+        g2 = [torch.zeros(n, device=DEV) for _ in range(3)]
+        y2 = F.acdc_forward(xs[i].to(DEV), a, d, b)
+        dx2 = F.acdc_backward(xs[i].to(DEV), dys[i].to(DEV), a, d, *g2)
+        torch.cuda.synchronize()
+        torch.testing.assert_close(ys[i], y2.cpu(), rtol=0, atol=0)
+        torch.testing.assert_close(dxs[i], dx2.cpu(), rtol=0, atol=0)
+        for u, v in zip(gs[i], g2):
+            torch.testing.assert_close(u, v, rtol=1e-5, atol=1e-4)
+
+
 @pytest.mark.parametrize("n,rows", [(1024, 4096), (4096, 2048)])
 def test_backward_of_forward_output_back_to_back(n, rows):
     """backward(dy = y) launched right after the forward that writes y: the
