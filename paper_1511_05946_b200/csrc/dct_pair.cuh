@@ -143,6 +143,9 @@ __device__ __forceinline__ void scatter_pairs_to_fft(const float2 (&gp)[G::E], f
 // so the pair exchanges are register shuffles, the DCT-II post-pass feeds
 // the DCT-III pre-pass without touching shared memory, and global rows are
 // moved as 64-bit pairs.  Butterflies 0 and S/2 are self-paired.
+#ifndef ACDC_FP_SELFSRC  // 1: frequency pairing shuffles from a per-lane source (no selects for the self-paired slots)
+#define ACDC_FP_SELFSRC 0
+#endif
 template <class G>
 struct FastMap {
   static constexpr int N = G::N;
@@ -152,6 +155,7 @@ struct FastMap {
   int jsp, jfq;                            // spatial / frequency butterfly
   bool isz, ish;                           // jfq == 0 / jfq == S/2
   unsigned mask;
+  int fsrc;                                // frequency partner lane (self for the two self-paired slots)
   __device__ __forceinline__ FastMap(int t, unsigned group_mask) {
     const int w = t / B, l = t % B;
     const int lo = H * w + l;
@@ -160,6 +164,11 @@ struct FastMap {
     jsp = l < H ? lo : S - 1 - H * w - (l - H);
     jfq = l < H ? lo : (ish ? S / 2 : S - H * w - (l - H));
     mask = group_mask;
+    const int lane = threadIdx.x & 31;
+    fsrc = (isz || ish) ? lane : (lane ^ H);
+  }
+  __device__ __forceinline__ float2 freq_shfl(float2 v) const {
+    return make_float2(__shfl_sync(mask, v.x, fsrc), __shfl_sync(mask, v.y, fsrc));
   }
   __device__ __forceinline__ float2 xor_shfl(float2 v) const {
     return make_float2(__shfl_xor_sync(mask, v.x, H), __shfl_xor_sync(mask, v.y, H));
@@ -177,6 +186,16 @@ struct FastMap {
 // Z[jfq + q*S] (q < 16, last-pass output) -> W[s] = Z[hi_s] for s < 8.
 template <class G>
 __device__ __forceinline__ void fp_partner(const float2 (&z)[16], float2 (&w)[8], const FastMap<G>& fm) {
+#if ACDC_FP_SELFSRC
+  // the self-paired slots shuffle from their own lane: slot 0 sends its own
+  // mirror values, slot S/2 receives what it sends
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const float2 self0 = s == 0 ? z[8] : z[(16 - s) & 15];
+    w[s] = fm.freq_shfl(fm.isz ? self0 : z[15 - s]);
+  }
+  return;
+#endif
   float2 r[8];
 #pragma unroll
   for (int s = 0; s < 8; ++s) r[s] = fm.xor_shfl(z[15 - s]);
@@ -191,6 +210,18 @@ __device__ __forceinline__ void fp_partner(const float2 (&z)[16], float2 (&w)[8]
 template <class G>
 __device__ __forceinline__ void fp_scatter(const float2 (&gl)[8], const float2 (&gh)[8], float2 (&v)[16],
                                            const FastMap<G>& fm) {
+#if ACDC_FP_SELFSRC
+  {
+    float2 r[8];
+#pragma unroll
+    for (int s = 0; s < 8; ++s) r[s] = fm.freq_shfl(fm.isz ? gh[s == 7 ? 0 : s + 1] : gh[s]);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) v[s] = gl[s];
+#pragma unroll
+    for (int q = 8; q < 16; ++q) v[q] = r[15 - q];
+    return;
+  }
+#endif
   float2 r[8];
 #pragma unroll
   for (int s = 0; s < 8; ++s) r[s] = fm.xor_shfl(gh[s]);
