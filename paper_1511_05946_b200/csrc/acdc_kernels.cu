@@ -650,13 +650,22 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
 #ifndef ACDC_TM_MAX_LOGN  // largest size with tables in smem (n = 16384 keeps them in global memory)
 #define ACDC_TM_MAX_LOGN 13
 #endif
+#ifndef ACDC_TM_NO_ASTASH  // 1: the TMEM backward reads a through L1 instead of a shared-memory stash
+#define ACDC_TM_NO_ASTASH 0
+#endif
+#ifndef ACDC_TM_NBUF  // exchange buffers per group in the TMEM backward (0: the plan's choice)
+#define ACDC_TM_NBUF 0
+#endif
+#ifndef ACDC_TM_FORCE_GTAB  // 1: the TMEM backward reads its tables from global memory (more L1, less smem)
+#define ACDC_TM_FORCE_GTAB 0
+#endif
 template <int LOGN>
-using GeoBwdTm = Geo<LOGN, 0, fp_gpc<LOGN, ACDC_BWD_TM_CTA>()>;
+using GeoBwdTm = Geo<LOGN, 0, fp_gpc<LOGN, ACDC_BWD_TM_CTA>(), ACDC_TM_FORCE_GTAB, ACDC_TM_NBUF>;
 // d stash [slot][t] float2 always; the a stash [q][t] float2 only where it fits
 template <int LOGN>
 __host__ __device__ constexpr bool bwd_tm_astash() {
   using G = GeoBwdTm<LOGN>;
-  return G::SMEM_BYTES + 2 * 8 * G::T * 8 <= G::SMEM_LIMIT;
+  return !ACDC_TM_NO_ASTASH && G::SMEM_BYTES + 2 * 8 * G::T * 8 <= G::SMEM_LIMIT;
 }
 template <int LOGN>
 __host__ __device__ constexpr int bwd_tm_stash_bytes() {
@@ -878,7 +887,13 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
   // their own (now idle) exchange buffers, group 0 adds them in group order.
   // ws[cta][0] = grad_a, [1] = grad_d, [2] = grad_bias.
   if constexpr (G::GPC > 1) {
-    static_assert(48 * T <= G::NBUF * G::BUF_FLOATS, "parking area");
+    // one exchange buffer: the last group's park runs on into the stashes,
+    // which the other groups may still be reading
+    constexpr bool ONE = G::NBUF == 1;
+    static_assert(ONE ? (G::GPC == 2 && 48 * T <= G::BUF_FLOATS + bwd_tm_stash_bytes<LOGN>() / 4)
+                      : 48 * T <= G::NBUF * G::BUF_FLOATS,
+                  "parking area");
+    if constexpr (ONE) __syncthreads();
     float* park = smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS + t;  // [col][T]
     if (c.grp > 0) {
 #pragma unroll
@@ -1242,6 +1257,9 @@ static LaunchInfo info_for(int kind) {
         li.pdl = true;  // prologue overlaps the forward's tail (pdl_wait before the h2 reads)
 #endif
         li.smem += bwd_tm_stash_bytes<LOGN>();
+#ifdef ACDC_TM_EXTRA_SMEM  // experiment: L1 capacity sensitivity
+        li.smem += ACDC_TM_EXTRA_SMEM;
+#endif
         li.max_per_sm = 512 / bwd_tm_cols<LOGN>();  // resident CTAs must not wait for TMEM columns
         break;
       }

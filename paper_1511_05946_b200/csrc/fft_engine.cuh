@@ -263,7 +263,7 @@ struct Plan {
 #ifndef ACDC_E32_FROM  // log2 N from which each thread holds 32 values (T = N / 32)
 #define ACDC_E32_FROM 15
 #endif
-template <int LOGN, int STASH = 0, int GPCX = 0>
+template <int LOGN, int STASH = 0, int GPCX = 0, bool GTAB = false, int NBUFX = 0>
 struct Geo : Plan<LOGN> {
   using P_ = Plan<LOGN>;
   static constexpr int N = 1 << LOGN;
@@ -285,8 +285,8 @@ struct Geo : Plan<LOGN> {
   static constexpr bool FIT_T2 = !SPLIT && bytes(true, 2, STASH_SMEM) <= SMEM_LIMIT;
   static constexpr bool FIT_T1 = bytes(true, 1, STASH_SMEM) <= SMEM_LIMIT;
   static constexpr bool FIT_G2 = !SPLIT && bytes(false, 2, STASH_SMEM) <= SMEM_LIMIT;
-  static constexpr bool TW_SMEM = FIT_T2 || FIT_T1;  // tables staged in smem?
-  static constexpr int NBUF = FIT_T2 ? 2 : (FIT_T1 ? 1 : (FIT_G2 ? 2 : 1));
+  static constexpr bool TW_SMEM = !GTAB && (FIT_T2 || FIT_T1);  // tables staged in smem?
+  static constexpr int NBUF = NBUFX ? NBUFX : (FIT_T2 ? 2 : (FIT_T1 ? 1 : (FIT_G2 ? 2 : 1)));
   static constexpr int TAB_FLOATS = TW_SMEM ? TAB_FULL : 0;
   static constexpr int SMEM_BYTES = bytes(TW_SMEM, NBUF, STASH_SMEM);
   static constexpr int GROUP_FLOATS = NBUF * BUF_FLOATS + (STASH_SMEM ? STASH_FLOATS : 0);
