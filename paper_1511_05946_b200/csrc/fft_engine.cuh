@@ -21,6 +21,7 @@
 // twiddles live in per-pass [q][k] tables and the padding function padi()
 // is split into base and offset parts below.
 #pragma once
+#include <type_traits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -477,8 +478,15 @@ __device__ __forceinline__ void pass_compute(float2 (&v)[G::E], const float2* tw
   }
 }
 
+// Exchange index: padded (the exchange after pass 0, whose writers are 16
+// slots apart) or plain (every later exchange: each half-warp writes and reads
+// 16 consecutive slots, and the frequency-pairing reads S-16w-15 ... S-16w
+// then stay on 16 distinct bank pairs).
+template <bool PAD>
+__device__ __forceinline__ constexpr int xi(int i) { return PAD ? padi(i) : i; }
+
 // Write the outputs of pass P at their autosorted positions.
-template <class G, int P, class PUT>
+template <class G, int P, class PUT, bool PAD = true>
 __device__ __forceinline__ void pass_store(const float2 (&v)[G::E], const PUT& put, int j0) {
   constexpr int R = G::radix(P);
   constexpr int NS = G::span(P);
@@ -487,34 +495,35 @@ __device__ __forceinline__ void pass_store(const float2 (&v)[G::E], const PUT& p
   for (int b = 0; b < NB; ++b) {
     const int j = j0 + b * G::T;
     const int k = j & (NS - 1);
-    const int pd = padi((j - k) * R + k);
+    const int pd = xi<PAD>((j - k) * R + k);
     if constexpr (NS == 1 && ACDC_PADS % 2 == 0 && PUT::kPair && R >= 2) {
 #pragma unroll
       for (int q = 0; q < R; q += 2) put.pair(pd + q, v[b * R + q], v[b * R + q + 1]);
     } else {
 #pragma unroll
-      for (int q = 0; q < R; ++q) put(pd + padoff(q * NS), v[b * R + q]);
+      for (int q = 0; q < R; ++q) put(pd + xi<PAD>(q * NS), v[b * R + q]);
     }
   }
 }
 
 // Read the inputs of pass P (stride N/R).
-template <class G, int P, class GET>
+template <class G, int P, class GET, bool PAD = true>
 __device__ __forceinline__ void pass_load(float2 (&v)[G::E], const GET& get, int j0) {
   constexpr int R = G::radix(P);
   constexpr int NB = G::E / R;
   constexpr int S = G::N / R;
-  const int pt = padi(j0);
+  const int pt = xi<PAD>(j0);
 #pragma unroll
   for (int b = 0; b < NB; ++b)
 #pragma unroll
-    for (int q = 0; q < R; ++q) get(pt + padoff(b * G::T) + padoff(q * S), v[b * R + q]);
+    for (int q = 0; q < R; ++q) get(pt + xi<PAD>(b * G::T) + xi<PAD>(q * S), v[b * R + q]);
 }
 
 // All passes of the FFT; v holds pass-0 inputs on entry and the natural-order
 // outputs of the last pass on exit (v[b*R_L + q] = X[j_b + q*N/R_L]).  Pass 0
-// uses butterfly base jf, the last pass jl, the others t.
-template <class G, int P = 0>
+// uses butterfly base jf, the last pass jl, the others t.  LATE_PAD = false:
+// the exchanges after pass 1, 2, ... use plain indices (see xi).
+template <class G, int P = 0, bool LATE_PAD = true>
 __device__ __forceinline__ void fft_passes(float2 (&v)[G::E], Xbuf<G>& xb, const GroupSync<G>& gs,
                                            const float2* tw, int t, int jf, int jl) {
   constexpr int L = G::NPASS - 1;
@@ -523,10 +532,11 @@ __device__ __forceinline__ void fft_passes(float2 (&v)[G::E], Xbuf<G>& xb, const
   if constexpr (P < L) {
     constexpr int PN = P + 1;
     const int jn = PN == L ? jl : t;
+    constexpr bool PAD = LATE_PAD || P == 0 || G::T < 16;
     xchg(
-        xb, gs, [&](const auto& put) { pass_store<G, P>(v, put, jp); },
-        [&](const auto& get) { pass_load<G, PN>(v, get, jn); });
-    fft_passes<G, PN>(v, xb, gs, tw, t, jf, jl);
+        xb, gs, [&](const auto& put) { pass_store<G, P, std::decay_t<decltype(put)>, PAD>(v, put, jp); },
+        [&](const auto& get) { pass_load<G, PN, std::decay_t<decltype(get)>, PAD>(v, get, jn); });
+    fft_passes<G, PN, LATE_PAD>(v, xb, gs, tw, t, jf, jl);
   }
 }
 template <class G>
