@@ -18,6 +18,9 @@
 #include "kernel_common.cuh"
 #include "runtime.h"
 
+#ifndef ACDC_CASCADE_LATE_PAD  // 0: the fused cascade forward's exchanges after pass 0 are unpadded
+#define ACDC_CASCADE_LATE_PAD 1
+#endif
 namespace acdc {
 
 struct CParams {
@@ -94,7 +97,7 @@ __global__ void ACDC_LB(Geo<LOGN>) cascade_fwd_kernel(CParams p) {
         }
         fp_from_pairs<G>(v, pa, pb, fm);
       }
-      fft_passes<G, 0>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
+      fft_passes<G, 0, ACDC_CASCADE_LATE_PAD>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
       {
         float2 w[8], gl[8], gh[8];
         fp_partner<G>(v, w, fm);
@@ -116,7 +119,7 @@ __global__ void ACDC_LB(Geo<LOGN>) cascade_fwd_kernel(CParams p) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) an[q] = ld_f2(pav + 2 * q * S);
       }
-      fft_passes<G, 0>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
+      fft_passes<G, 0, ACDC_CASCADE_LATE_PAD>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
       fp_out_pairs<G>(v, pa, pb, fm);  // ACDC_l output pairs
       const int fl = p.flags ? p.flags[l] : 0;
       if (fl & 1) {  // ReLU, strict x > 0 (layers.py:227)
@@ -191,6 +194,8 @@ static int cinfo_for(int logn, LaunchInfo* li) {
     case 12: *li = cinfo<12>(); return ACDC_OK;
     case 13: *li = cinfo<13>(); return ACDC_OK;
     case 14: *li = cinfo<14>(); return ACDC_OK;
+#elif ACDC_ONLY_LOGN >= 8 && ACDC_ONLY_LOGN <= 14
+    case ACDC_ONLY_LOGN: *li = cinfo<ACDC_ONLY_LOGN>(); return ACDC_OK;
 #endif
     default:
       return set_error(ACDC_E_SIZE, "the fused cascade needs 256 <= n <= 16384");
