@@ -656,6 +656,12 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
 #ifndef ACDC_TM_NO_ASTASH  // 1: the TMEM backward reads a through L1 instead of a shared-memory stash
 #define ACDC_TM_NO_ASTASH 0
 #endif
+#ifndef ACDC_TM_LATE_PAD1  // padded exchanges after pass 0 in the TMEM backward's dy / g1 transforms
+#define ACDC_TM_LATE_PAD1 1
+#endif
+#ifndef ACDC_TM_LATE_PAD2
+#define ACDC_TM_LATE_PAD2 1
+#endif
 #ifndef ACDC_TM_NBUF  // exchange buffers per group in the TMEM backward (0: the plan's choice)
 #define ACDC_TM_NBUF 0
 #endif
@@ -791,7 +797,7 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
     } else {
       fp_load<G, false>(v, p.dy + ra * p.ldy, hasb ? p.dy + (ra + 1) * p.ldy : nullptr, nullptr, fm);
     }
-    fft_passes<G, 0>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
+    fft_passes<G, 0, ACDC_TM_LATE_PAD1>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
     {
       float2 w[8], gl[8], gh[8];
       fp_partner<G>(v, w, fm);
@@ -830,7 +836,7 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
         xbv[q] = ld_row_f2(pxb + 2 * q * S);  // row rb == ra when !hasb: in bounds, unused
       }
     }
-    fft_passes<G, 0>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
+    fft_passes<G, 0, ACDC_TM_LATE_PAD2>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
     // exchange 4 has passed: buffer A (last read at exchange 3) takes the next dy
     if (staged && t == 0 && it + c.gstride < npairs) issue_dy(rmap(it + c.gstride));
     float2 ga[8], gb[8];
