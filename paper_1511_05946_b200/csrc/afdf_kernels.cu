@@ -21,6 +21,12 @@
 #include "runtime.h"
 #include "tmem.cuh"
 
+#ifndef ACDC_AFDF_LATE_PAD  // 0: AFDF / row-FFT exchanges after pass 0 unpadded (C5 forward: +0.4%, stays padded)
+#define ACDC_AFDF_LATE_PAD 1
+#endif
+#ifndef ACDC_AFDF_BWD_LATE_PAD  // the TMEM AFDF backward: unpadded after pass 0 (C5 backward -1.6%)
+#define ACDC_AFDF_BWD_LATE_PAD 0
+#endif
 namespace acdc {
 
 struct FParams {
@@ -108,7 +114,7 @@ __global__ void ACDC_LB(Geo<LOGN>) afdf_fwd_kernel(FParams p) {
     for (int b = 0; b < E / R0; ++b)
 #pragma unroll
       for (int q = 0; q < R0; ++q) v[b * R0 + q] = cmul(__ldg(xr + fpos<G, 0>(b, q)), ld_param(ar + fpos<G, 0>(b, q)));
-    fft_passes<G>(v, xb, gs, tw, t);
+    fft_passes<G, 0, ACDC_AFDF_LATE_PAD>(v, xb, gs, tw, t, t, t);
     // V = conj(d * X) at the last-pass slots
     const float2* dr = p.d + t;
 #pragma unroll
@@ -116,7 +122,7 @@ __global__ void ACDC_LB(Geo<LOGN>) afdf_fwd_kernel(FParams p) {
 #pragma unroll
       for (int q = 0; q < RL; ++q) v[b * RL + q] = conjf2(cmul(v[b * RL + q], ld_param(dr + fpos<G, PL>(b, q))));
     last_to_first<G>(v, xb, gs, t);
-    fft_passes<G>(v, xb, gs, tw, t);
+    fft_passes<G, 0, ACDC_AFDF_LATE_PAD>(v, xb, gs, tw, t, t, t);
     float2* yr = p.y + r * p.ldo + t;
 #pragma unroll
     for (int b = 0; b < E / RL; ++b)
@@ -204,7 +210,7 @@ __global__ void ACDC_LB(GeoFT<LOGN>) afdf_fwd_tm_kernel(FParams p) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) v[8 * half + j] = cmul(xn[8 * half + j], av[j]);
     }
-    fft_passes<G>(v, xb, gs, tw, t);
+    fft_passes<G, 0, ACDC_AFDF_LATE_PAD>(v, xb, gs, tw, t, t, t);
     // V = conj(d * X)
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
@@ -217,7 +223,7 @@ __global__ void ACDC_LB(GeoFT<LOGN>) afdf_fwd_tm_kernel(FParams p) {
 #pragma unroll
       for (int q = 0; q < 16; ++q) xn[q] = __ldg(p.x + (r + gstride) * p.ldx + t + q * T);
     }
-    fft_passes<G>(v, xb, gs, tw, t);
+    fft_passes<G, 0, ACDC_AFDF_LATE_PAD>(v, xb, gs, tw, t, t, t);
     float2* yr = p.y + r * p.ldo + t;
 #pragma unroll
     for (int q = 0; q < 16; ++q) yr[q * T] = make_float2(v[q].x * scale, -v[q].y * scale);
@@ -254,7 +260,7 @@ __global__ void ACDC_LB(Geo<LOGN>) fft_rows_kernel(FParams p) {
         const float2 z = ld_param(xr + fpos<G, 0>(b, q));
         v[b * R0 + q] = INV ? conjf2(z) : z;
       }
-    fft_passes<G>(v, xb, gs, tw, t);
+    fft_passes<G, 0, ACDC_AFDF_LATE_PAD>(v, xb, gs, tw, t, t, t);
     float2* yr = p.y + r * p.ldo + t;
 #pragma unroll
     for (int b = 0; b < E / RL; ++b)
@@ -301,7 +307,7 @@ __global__ void ACDC_LB(GeoF<LOGN>) afdf_bwd_kernel(FParams p) {
     for (int b = 0; b < E / R0; ++b)
 #pragma unroll
       for (int q = 0; q < R0; ++q) v[b * R0 + q] = cmul(__ldg(xr + fpos<G, 0>(b, q)), ld_param(p.a + t + fpos<G, 0>(b, q)));
-    fft_passes<G>(v, xb, gs, tw, t);
+    fft_passes<G, 0, ACDC_AFDF_LATE_PAD>(v, xb, gs, tw, t, t, t);
 #pragma unroll
     for (int i = 0; i < E; ++i) st_h[i * T] = conjf2(v[i]);
     // g = FFT(dy): grad_d partial += g * conj(h2) (1/N applied at the end)
@@ -310,7 +316,7 @@ __global__ void ACDC_LB(GeoF<LOGN>) afdf_bwd_kernel(FParams p) {
     for (int b = 0; b < E / R0; ++b)
 #pragma unroll
       for (int q = 0; q < R0; ++q) v[b * R0 + q] = __ldg(dyr + fpos<G, 0>(b, q));
-    fft_passes<G>(v, xb, gs, tw, t);
+    fft_passes<G, 0, ACDC_AFDF_LATE_PAD>(v, xb, gs, tw, t, t, t);
 #pragma unroll
     for (int b = 0; b < E / RL; ++b)
 #pragma unroll
@@ -322,7 +328,7 @@ __global__ void ACDC_LB(GeoF<LOGN>) afdf_bwd_kernel(FParams p) {
         v[i] = cmul(conjf2(v[i]), ld_param(p.d + t + fpos<G, PL>(b, q)));
       }
     last_to_first<G>(v, xb, gs, t);
-    fft_passes<G>(v, xb, gs, tw, t);
+    fft_passes<G, 0, ACDC_AFDF_LATE_PAD>(v, xb, gs, tw, t, t, t);
     const float scale = 1.0f / G::N;
     float2* oxr = p.y + r * p.ldo + t;
 #pragma unroll
@@ -413,7 +419,7 @@ __global__ void ACDC_LB(GeoFT<LOGN>) afdf_bwd_tm_kernel(FParams p) {
     }
 #pragma unroll
     for (int q = 0; q < 16; ++q) v[q] = cmul(v[q], ast[q * T]);
-    fft_passes<G>(v, xb, gs, tw, t);  // h2 = FFT(a x)
+    fft_passes<G, 0, ACDC_AFDF_BWD_LATE_PAD>(v, xb, gs, tw, t, t, t);  // h2 = FFT(a x)
     {
       float2 h[8];
 #pragma unroll
@@ -425,7 +431,7 @@ __global__ void ACDC_LB(GeoFT<LOGN>) afdf_bwd_tm_kernel(FParams p) {
     }
 #pragma unroll
     for (int q = 0; q < 16; ++q) v[q] = g[q];
-    fft_passes<G>(v, xb, gs, tw, t);  // g = FFT(dy)
+    fft_passes<G, 0, ACDC_AFDF_BWD_LATE_PAD>(v, xb, gs, tw, t, t, t);  // g = FFT(dy)
     // grad_d partial += g * conj(h2);  V = conj(g) * d
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
@@ -444,7 +450,7 @@ __global__ void ACDC_LB(GeoFT<LOGN>) afdf_bwd_tm_kernel(FParams p) {
 #pragma unroll
       for (int q = 0; q < 16; ++q) xn[q] = __ldg(p.x + (r + gstride) * p.ldx + t + q * T);
     }
-    fft_passes<G>(v, xb, gs, tw, t);  // g1 = conj(FFT(V)) / N  (times N: the 1/N cancels, see header)
+    fft_passes<G, 0, ACDC_AFDF_BWD_LATE_PAD>(v, xb, gs, tw, t, t, t);  // g1 = conj(FFT(V)) / N  (times N: the 1/N cancels, see header)
     float2* oxr = p.y + r * p.ldo + t;
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
