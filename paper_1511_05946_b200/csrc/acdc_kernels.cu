@@ -158,6 +158,7 @@ __host__ __device__ constexpr int fwd_pstash_bytes() {
 #ifndef ACDC_FWD_LATE_PAD  // 0: the forward's exchanges after pass 0 are unpadded (fwd -1.3%; the backward
 #define ACDC_FWD_LATE_PAD 0  // kernels measured +3% with it and keep the padded layout)
 #endif
+// (N = 8192 keeps the padded layout: its 16 x 2 x 16 x 16 plan measured +0.6% unpadded)
 #ifndef ACDC_FWD_LATE_PAD1  // per transform: h2 = DCT(a x), y = IDCT(d h2 + b)
 #define ACDC_FWD_LATE_PAD1 ACDC_FWD_LATE_PAD
 #endif
@@ -201,7 +202,7 @@ __global__ void ACDC_LB(GeoFwd<LOGN>) acdc_fwd_kernel(KParams p) {
       }
       float2 v[16];
       fp_load<G, true>(v, p.x + ra * p.ldx, hasb ? p.x + (ra + 1) * p.ldx : nullptr, p.a, fm);
-      fft_passes<G, 0, ACDC_FWD_LATE_PAD1>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
+      fft_passes<G, 0, ACDC_FWD_LATE_PAD1 || LOGN == 13>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
       {
         float2 w[8], gl[8], gh[8];
         fp_partner<G>(v, w, fm);
@@ -233,7 +234,7 @@ __global__ void ACDC_LB(GeoFwd<LOGN>) acdc_fwd_kernel(KParams p) {
         }
         fp_scatter<G>(gl, gh, v, fm);
       }
-      fft_passes<G, 0, ACDC_FWD_LATE_PAD2>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
+      fft_passes<G, 0, ACDC_FWD_LATE_PAD2 || LOGN == 13>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
       float2 oa[8], ob[8];
       fp_out_pairs<G>(v, oa, ob, fm);
       float2* ya = reinterpret_cast<float2*>(p.y + ra * p.ldo + 2 * fm.jsp);
