@@ -3,12 +3,21 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU, NCCL)
 
-A step is one pass of the hot path over one batch: forward (y = C3(d*C2(a*x)+b)),
-backward (dx and the three diagonal gradients, h2 recomputed), the fixed-order
-gradient reduction, and for N > 1 the NCCL all-reduce of the flat [ga|gd|gb]
-gradient buffer.  Batch 16384 rows per GPU (weak scaling).  Inputs are
-synthetic Gaussian fp32 tensors resident in HBM (each 256 MiB > the 126 MB
-L2, so no L2 flush is needed between steps).
+A step is one pass of the hot path over one batch through the reference-shaped
+layer API: ``AcdcLayer.forward`` (y = C3(d*C2(a*x)+b)), ``AcdcLayer.backward``
+(dx and the three diagonal gradients, accumulated), the fixed-order gradient
+reduction, and ``DataParallel.allreduce_grads`` (for N > 1 one NCCL all-reduce
+of the flat [ga|gd|gb] gradient buffer).  Batch 16384 rows per GPU (weak
+scaling, the default) or 16384 rows in total (``--scaling strong``).  Inputs
+are synthetic Gaussian fp32 tensors resident in HBM (each 256 MiB > the
+126 MB L2, so no L2 flush is needed between steps).
+
+``--gpus N`` without a torchrun environment re-launches itself under
+``torch.distributed.run`` with N ranks (one process per GPU, NCCL).
+
+Roofline: algorithmic bytes per row are 8N for the forward,
+12N for the backward (x, dy in, dx out) and 20N per step; the h2 cache the
+kernels may keep (+4N out, +4N in) is reported as moved bytes, not counted.
 
 ``--impl reference`` times the reference's own compiled CPU kernels
 (``oracle/_ref``, the Cython ``_kernels.pyx`` built from /root/reference) on
@@ -51,6 +60,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: --batch rows per GPU; strong: --batch rows in total, sharded over the ranks")
     ap.add_argument("--mode", default="auto", choices=["auto", "recompute", "h2cache"],
                     help="recompute h2 in the backward (PAPER.md:275) or cache it from the forward "
                          "(layers.py:145); auto times both and reports the faster")
@@ -190,16 +201,48 @@ def reference_cpu(n, threads, rows, seconds=None, steps=None, warmup=0):
 
 
 # ------------------------------------------------------------------ our arm
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(gpus: int, script: str) -> None:
+    """``--gpus N`` (N > 1) outside torchrun: re-run this script under
+    ``torch.distributed.run`` with N ranks on this node and exit with its code
+    (rank 0 prints the JSON line)."""
+    if gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(script), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def dist_setup(gpus):
+    """One process per GPU.  ``ACDC_DIST_BACKEND=gloo`` + ``ACDC_SHARE_GPU=1``
+    put every rank on cuda:0 (exercises the multi-rank path on a 1-GPU box;
+    NCCL refuses two ranks on one device)."""
     import torch
     import torch.distributed as dist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if gpus > 1 and world != gpus:
+        raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={world}")
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        share = os.environ.get("ACDC_SHARE_GPU") == "1"
+        ndev = torch.cuda.device_count()
+        if not share and world > ndev:
+            raise SystemExit(f"{world} ranks but only {ndev} visible GPUs")
+        dev = 0 if share else local
+        torch.cuda.set_device(dev)
+        backend = os.environ.get("ACDC_DIST_BACKEND", "nccl")
+        kw = {"device_id": torch.device("cuda", dev)} if backend == "nccl" else {}
+        dist.init_process_group(backend, **kw)
+        local = dev
     else:
         torch.cuda.set_device(0)
     return world, rank, local
@@ -229,42 +272,53 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1511_05946_b200 import _lib, functional as F
+    from paper_1511_05946_b200 import AcdcLayer, _lib, functional as F
+    from paper_1511_05946_b200.parallel import DataParallel, shard_rows
 
     world, rank, local = dist_setup(args.gpus)
-    n, B = args.n, args.batch
+    n = args.n
+    if args.scaling == "strong":  # --batch rows in total, contiguous shards
+        lo, hi = shard_rows(args.batch, world, rank)
+        B = hi - lo
+        global_rows = args.batch
+    else:
+        B = args.batch
+        global_rows = B * world
     dev = torch.device("cuda", torch.cuda.current_device())
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
     x = torch.randn(B, n, device=dev, generator=g)
     dy = torch.randn(B, n, device=dev, generator=g)
+    g.manual_seed(99)  # replicated parameters: the same seed on every rank
     a = 1 + 0.1 * torch.randn(n, device=dev, generator=g)
     d = 1 + 0.1 * torch.randn(n, device=dev, generator=g)
     bias = 0.1 * torch.randn(n, device=dev, generator=g)
-    if world > 1:  # replicated parameters
-        for p in (a, d, bias):
-            dist.broadcast(p, 0)
-    grads = torch.zeros(3, n, device=dev)
-    y = torch.empty_like(x)
-    dx = torch.empty_like(x)
     F.prepare(n, dev)
     stream = torch.cuda.current_stream()
-    cache = F.new_h2cache(B, n, dev) if F.h2cache_supported(n) else None
+
+    def make(mode):
+        """The reference-shaped layer (layers.py:108-156) wrapped for data
+        parallelism: grads live in one flat buffer, one all-reduce per step."""
+        layer = AcdcLayer(n, device=dev, cache_h2=(mode == "h2cache"))
+        layer.a.copy_(a)
+        layer.d.copy_(d)
+        layer.bias_d.copy_(bias)
+        return DataParallel(layer)
 
     def timed(mode):
         """W warm-up + exactly K timed steps of one mode; per-kernel CUDA events."""
-        hc = cache if mode == "h2cache" else None
+        dp = make(mode)
         ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
 
         def step(i=None):
             e = ev[i] if i is not None else None
+            dp.zero_grads()
             if e: e[0].record(stream)
-            F.acdc_forward(x, a, d, bias, out=y, h2cache=hc)
+            dp.forward(x)
             if e: e[1].record(stream)
-            F.acdc_backward(x, dy, a, d, grads[0], grads[1], grads[2], accumulate=False, out=dx, h2cache=hc)
+            dp.backward(dy)
             if e: e[2].record(stream)
-            if world > 1:
-                dist.all_reduce(grads)
+            dp.allreduce_grads()
             if e: e[3].record(stream)
 
         for _ in range(max(args.warmup, 3)):
@@ -286,17 +340,21 @@ def run_ours(args):
         for i in range(args.steps):  # per-kernel split, outside the timed region
             step(i)
         torch.cuda.synchronize()
-        return {
+        res = {
             "mode": mode,
             "max_ms": max_ms,
             "fwd_ms": sum(e[0].elapsed_time(e[1]) for e in ev) / args.steps,
             "bwd_ms": sum(e[1].elapsed_time(e[2]) for e in ev) / args.steps,
             "ar_ms": sum(e[2].elapsed_time(e[3]) for e in ev) / args.steps,
             "clocks": clocks,
-            "value": world * B * args.steps / (max_ms / 1e3),
+            "value": global_rows * args.steps / (max_ms / 1e3),
+            "grads_finite": bool(torch.isfinite(dp.flat).all()),
         }
+        del dp
+        torch.cuda.empty_cache()
+        return res
 
-    modes = ["recompute"] if (cache is None or args.mode == "recompute") else (
+    modes = ["recompute"] if (not F.h2cache_supported(n) or args.mode == "recompute") else (
         ["h2cache"] if args.mode == "h2cache" else ["recompute", "h2cache"])
     runs = [timed(m) for m in modes]
     best = max(runs, key=lambda r: r["value"])
@@ -305,15 +363,16 @@ def run_ours(args):
     max_ms = best["max_ms"]
     ms_per_step = max_ms / args.steps
     value = best["value"]
-    # bytes per row moved by each kernel in the chosen mode (h2 cache adds 4N out + 4N in)
+    # algorithmic bytes per row: fwd 8N, bwd 12N; the h2 cache adds 4N out + 4N in (moved, not counted)
     cache_b = 4 * n if best["mode"] == "h2cache" else 0
-    bytes_fwd, bytes_bwd = 8 * n + cache_b, 12 * n + cache_b
+    alg_fwd, alg_bwd = 8 * n, 12 * n
+    mov_fwd, mov_bwd = alg_fwd + cache_b, alg_bwd + cache_b
 
     # e2e through the public API with host buffers (pinned), copies in the timed region
     e2e = None
     if not args.no_e2e:
         e2e = e2e_measure(F, n, B, a, d, bias, dev, world, steps=max(3, min(args.steps, 10)),
-                          h2cache=cache if best["mode"] == "h2cache" else None)
+                          h2cache=best["mode"] == "h2cache", global_rows=global_rows)
 
     dense = None
     if not args.no_dense and rank == 0:
@@ -326,17 +385,18 @@ def run_ours(args):
         # h2-cache backward is the TMEM kernel for 512 <= n <= 8192 (acdc_kernels.cu bwd_tm_ok)
         if bwd_ms >= fwd_ms:
             bk = "acdc_bwd_tm_kernel" if (best["mode"] == "h2cache" and 512 <= n <= 8192) else "acdc_bwd_kernel"
-            kname, kms, kbytes = f"{bk}(+grad_reduce)", bwd_ms, bytes_bwd * B
+            kname, kms, kalg, kmov = f"{bk}(+grad_reduce)", bwd_ms, alg_bwd * B, mov_bwd * B
         else:
-            kname, kms, kbytes = "acdc_fwd_kernel", fwd_ms, bytes_fwd * B
-        achieved = kbytes / (kms / 1e3) / 1e9
-        step_bytes = (BYTES_FWD + BYTES_BWD) * n // N_FEAT * B
-        step_gbs = step_bytes / ((fwd_ms + bwd_ms) / 1e3) / 1e9
+            kname, kms, kalg, kmov = "acdc_fwd_kernel", fwd_ms, alg_fwd * B, mov_fwd * B
+        achieved = kalg / (kms / 1e3) / 1e9
+        step_alg = (alg_fwd + alg_bwd) * B
+        step_gbs = step_alg / (ms_per_step / 1e3) / 1e9
         traffic = None
         tpath = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tpath):
             try:
-                traffic = json.load(open(tpath)).get(kname.split("(")[0])
+                t = json.load(open(tpath)).get(kname.split("(")[0])
+                traffic = t * B / 16384 if (t is not None and n == N_FEAT) else None
             except Exception:
                 traffic = None
         out = {
@@ -348,17 +408,19 @@ def run_ours(args):
             "warmup": max(args.warmup, 3),
             "ms_per_step": ms_per_step,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": args.scaling,
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic Gaussian x, dy ~ N(0,1); a, d ~ N(1, 0.1^2); bias ~ N(0, 0.1^2)",
             "config": {
-                "workload": f"single ACDC layer fwd+bwd, N={n}, batch {B} rows per GPU, fp32",
+                "workload": f"single ACDC layer fwd+bwd (AcdcLayer under DataParallel), N={n}, "
+                            + (f"batch {B} rows per GPU" if args.scaling == "weak" else f"batch {args.batch} in total")
+                            + ", fp32",
                 "n": n,
                 "rows_per_gpu": B,
-                "global_rows": B * world,
+                "global_rows": global_rows,
                 "parallelism": f"dp{world}" if world > 1 else "single",
-                "l2": "inputs larger than L2 (x, dy, y, dx are 256 MiB each); no flush",
+                "l2": "inputs larger than L2 (x, dy, y, dx are 256 MiB each at B=16384); no flush",
             },
             "roofline": {
                 "kernel": kname,
@@ -369,7 +431,11 @@ def run_ours(args):
                 "unit": "GB/s",
                 "frac": achieved / hbm,
                 "traffic": traffic,
-                "algorithmic_bytes_per_launch": kbytes,
+                "algorithmic_bytes_per_launch": kalg,
+                "algorithmic_bytes_per_row": kalg // B,
+                "moved_bytes_per_launch": kmov,
+                "moved_frac": kmov / (kms / 1e3) / 1e9 / hbm,
+                "traffic_over_algorithmic": (traffic / kalg) if traffic else None,
                 "avg_launch_ms": kms,
                 "timing": "CUDA events around each kernel over K further steps right after the timed loop "
                           "(events between the kernels inside the timed loop would break the forward -> "
@@ -378,8 +444,8 @@ def run_ours(args):
             "mode": best["mode"],
             "other_modes": [{k: r[k] for k in ("mode", "value", "fwd_ms", "bwd_ms")} for r in other],
             "roofline_step": {
-                "bytes_per_row": (BYTES_FWD + BYTES_BWD) * n // N_FEAT,
-                "bytes_moved_per_row": bytes_fwd + bytes_bwd,
+                "bytes_per_row": alg_fwd + alg_bwd,
+                "bytes_moved_per_row": mov_fwd + mov_bwd,
                 "achieved_gbs": step_gbs,
                 "frac": step_gbs / hbm,
                 "fwd_ms": fwd_ms,
@@ -387,9 +453,11 @@ def run_ours(args):
                 "allreduce_ms": ar_ms,
             },
             "clocks": clocks,
-            # fwd + bwd + its one- or two-stage grad reduction per step (this arm's timed region)
+            # our kernels per step: fwd + bwd + its one- or two-stage grad reduction (the zero_grads
+            # memset is torch's, not counted)
             "gpu_launches": (1 + _lib.load().acdc_bwd_launch_count(B, n, 1 if best["mode"] == "h2cache" else 0))
             * args.steps,
+            "grads_finite": best["grads_finite"],
             "e2e": e2e,
             "dense_cublas": dense,
         }
@@ -403,7 +471,7 @@ def run_ours(args):
     return out
 
 
-def e2e_measure(F, n, B, a, d, bias, dev, world, steps, h2cache=None):
+def e2e_measure(F, n, B, a, d, bias, dev, world, steps, h2cache=False, global_rows=None):
     """Rows/s through the public API with pinned HOST buffers: per step the
     host->device copy of x and dy, forward, backward, and the device->host
     copy of y, dx and the gradients are all inside the timed region.  Uses
@@ -418,7 +486,7 @@ def e2e_measure(F, n, B, a, d, bias, dev, world, steps, h2cache=None):
     dxh = torch.empty(B, n).pin_memory()
     gh = torch.empty(3, n).pin_memory()
     grads = torch.zeros(3, n, device=dev)
-    pipe = F.HostPipeline(n, B, dev, chunks=4, h2cache=h2cache is not None)  # scripts/e2e_sweep.py
+    pipe = F.HostPipeline(n, B, dev, chunks=4, h2cache=h2cache)  # scripts/e2e_sweep.py
 
     def step():
         pipe.step(xh, dyh, yh, dxh, a, d, bias, (grads[0], grads[1], grads[2]), accumulate=False)
@@ -438,7 +506,7 @@ def e2e_measure(F, n, B, a, d, bias, dev, world, steps, h2cache=None):
     barrier(world)
     ms = max_over_ranks(t0.elapsed_time(t1), world)
     return {
-        "value": world * B * steps / (ms / 1e3),
+        "value": (global_rows or world * B) * steps / (ms / 1e3),
         "unit": UNIT,
         "h2d_bytes_per_step": 2 * B * n * 4,
         "d2h_bytes_per_step": 2 * B * n * 4 + 3 * n * 4,
@@ -481,12 +549,22 @@ def dense_measure(n, B, dev):
 
 
 def run_reference(args):
+    """The reference's own compiled CPU kernels (oracle/_ref: _kernels.pyx built
+    from /root/reference) driven with the reference layer's call sequence
+    (layers.py:141-156), rows sharded over all host threads.  Each step is the
+    full batch when the whole run fits in ~3 minutes at the measured rate,
+    else a contiguous row sample of it (CPU rows/s does not depend on the batch
+    size at N=4096: every row is an independent transform pair)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
     thr = cpu_threads()
-    rows = max(512, 32 * thr)
+    full = args.batch * (world if args.scaling == "weak" else 1)
+    rate, _, _, _, _ = reference_cpu(args.n, thr, max(512, 32 * thr), steps=1, warmup=1)  # calibration
+    budget_s = 150.0
+    rows = int(min(full, max(512, rate * budget_s / max(1, args.steps + args.warmup))))
+    rows -= rows % 2
     rps, kind, sample, times, used = reference_cpu(args.n, thr, rows, steps=args.steps, warmup=args.warmup)
     ms = 1e3 * sum(times) / len(times)
     return {
@@ -499,12 +577,16 @@ def run_reference(args):
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling,
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic Gaussian",
-        "config": {"workload": f"single ACDC layer fwd+bwd, N={args.n}, reference CPU path on {rows}-row samples",
-                   "n": args.n, "rows_per_step": rows},
+        "config": {"workload": f"single ACDC layer fwd+bwd, N={args.n}, reference CPU path, "
+                               f"{rows} of the {full} rows per step" + (" (full batch)" if rows == full else
+                                                                        " (row sample; rows/s is batch-invariant)"),
+                   "n": args.n, "rows_per_step": rows, "batch": full,
+                   "tables": "Makhoul tables from oracle.acdc_oracle.tables (transforms.py:86-122 restated, pinned "
+                             "against the reference's golden vectors)"},
         "cpu_baseline": {"value": rps, "unit": UNIT, "cores": used, "kind": kind, "sample": sample},
         "e2e": {"value": rps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -512,6 +594,7 @@ def run_reference(args):
 
 def main():
     args = parse()
+    maybe_spawn(args.gpus, __file__)
     if args.impl == "reference":
         out = run_reference(args)
     else:

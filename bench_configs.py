@@ -8,10 +8,14 @@ sweep single layer N=128..32768, batch 16384: rows/s and % of the 20N HBM
       roofline, next to a cuBLAS dense linear of the same N (fp32 and TF32)
 C3    12-block ACDC+ReLU+Perm cascade, N=1024, batch 8192: fused vs per-layer
 C4    deep SELL training step: 32 ACDC layers at N=4096 (fused cascade), MSE
-      loss gradient and momentum SGD on the diagonals, batch 4096 per GPU
-C5    complex AFDF N=8192, 8192 rows per GPU (65536 over 8 GPUs)
-Timing: CUDA events around K steps after warm-up; inputs larger than L2 or
-already L2-resident as stated per line.
+      loss gradient and momentum SGD on the diagonals, batch 4096 per GPU,
+      data-parallel over the ranks (bucketed all-reduce overlapping the backward)
+C5    complex AFDF N=8192, 65536 rows in total sharded over the ranks
+Timing: CUDA events around K steps after warm-up, max over ranks; inputs
+larger than L2 or already L2-resident as stated per line.
+
+    python bench_configs.py --only c4,c5 --gpus 8     (re-launches under torchrun)
+C4 / C5 run one process per GPU (NCCL); the other configs run on rank 0 only.
 """
 
 from __future__ import annotations
@@ -174,68 +178,142 @@ def c3(args, dev):
             "fused_hbm_frac": B / (ms_f / 1e3) * bytes_row / (peak_hbm() * 1e9)}
 
 
+def _dist():
+    import torch.distributed as dist
+
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    return world, rank
+
+
+def timeit_dist(fn, steps, warmup=3):
+    """CUDA-event time per step, barrier on both sides, max over ranks."""
+    import torch.distributed as dist
+
+    from bench import barrier, max_over_ranks
+
+    world, _ = _dist()
+    for _ in range(warmup):
+        fn()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    barrier(world)
+    return max_over_ranks(e0.elapsed_time(e1), world) / steps
+
+
 def c4(args, dev):
-    """Deep SELL step: forward, MSE loss gradient, backward, momentum SGD (training.py:72-84)."""
-    n, depth, B = 4096, 32, 4096
-    rng = np.random.default_rng(1)
-    casc, layers = _cascade(n, depth, False, dev, rng)
-    x = torch.randn(B, n, device=dev)
-    target = torch.randn(B, n, device=dev)
+    """Deep SELL step: forward, MSE loss gradient, backward, momentum SGD
+    (training.py:72-84, 210-249), batch-sharded: B rows per rank, parameters
+    replicated, gradients summed by DataParallel (one bucketed all-reduce whose
+    buckets overlap the backward of the earlier blocks)."""
+    from paper_1511_05946_b200.parallel import DataParallel
     from paper_1511_05946_b200.training import Sgd, SgdConfig
 
+    world, rank = _dist()
+    n, depth, B = 4096, 32, 4096
+    rng = np.random.default_rng(1)  # same parameters on every rank
+    casc, layers = _cascade(n, depth, False, dev, rng)
+    torch.manual_seed(1)
+    for l in layers:  # replicated init (normal_ above used the global generator)
+        l.a.normal_(1.0, 0.061)
+        l.d.normal_(1.0, 0.061)
+    g = torch.Generator(device=dev)
+    g.manual_seed(100 + rank)
+    x = torch.randn(B, n, device=dev, generator=g)
+    target = torch.randn(B, n, device=dev, generator=g)
+    dp = DataParallel(casc, bucket_bytes=(args.bucket_kib << 10) if world > 1 else None)
     opt = Sgd(casc.params(), SgdConfig(learning_rate=1e-3, momentum=0.9))  # training.py:58-84
+    scale = 2.0 / (B * world * n)  # mse over the global batch (training.py:176-183)
 
     def step():
-        y = casc.forward(x)
-        gy = (2.0 / y.numel()) * (y - target)  # mse_loss gradient (training.py:176-183)
-        casc.backward(gy)
-        opt.step()  # momentum SGD, zeroes the grads
+        y = dp.forward(x)
+        gy = scale * (y - target)
+        dp.backward(gy)
+        dp.allreduce_grads()
+        opt.step()  # momentum SGD on the summed grads, zeroes them
 
-    def step_fused():  # the SGD update inside each block's gradient reduction (acdc_bwd_sgd_f32)
+    def step_fused():  # 1 rank only: the SGD update inside each block's gradient reduction
         y = casc.forward(x)
-        gy = (2.0 / y.numel()) * (y - target)
+        gy = scale * (y - target)
         opt.backward_step(casc, gy)
 
-    ms = timeit(step, max(3, args.steps // 10))
-    ms_f = timeit(step_fused, max(3, args.steps // 10))
-    return {"config": "C4 deep SELL 32 ACDC layers N=4096 train step (1 GPU of the DP job)", "fused": casc.fused,
-            "batch_per_gpu": B, "ms_per_step": ms, "rows_per_s": B / (ms / 1e3),
-            "layer_rows_per_s": B * depth / (ms / 1e3),
-            "fused_sgd": {"ms_per_step": ms_f, "rows_per_s": B / (ms_f / 1e3)}}
+    ms = timeit_dist(step, max(3, args.steps // 10))
+    res = {"config": f"C4 deep SELL 32 ACDC layers N=4096 train step, {world} GPU(s) data-parallel",
+           "n_gpus": world, "fused": casc.fused, "batch_per_gpu": B, "global_batch": B * world, "ms_per_step": ms,
+           "rows_per_s": B * world / (ms / 1e3), "layer_rows_per_s": B * world * depth / (ms / 1e3),
+           "allreduce": (f"bucketed {args.bucket_kib} KiB, overlapping the backward" if world > 1 else "none"),
+           "scaling": "weak"}
+    if world == 1:
+        ms_f = timeit(step_fused, max(3, args.steps // 10))
+        res["fused_sgd"] = {"ms_per_step": ms_f, "rows_per_s": B / (ms_f / 1e3)}
+    return res
 
 
 def c5(args, dev):
-    n, B = 8192, 8192
-    x = torch.randn(B, n, dtype=torch.complex64, device=dev)
-    dy = torch.randn(B, n, dtype=torch.complex64, device=dev)
-    a = (1 + 0.1 * torch.randn(n, device=dev)) + 0.1j * torch.randn(n, device=dev)
-    d = (1 + 0.1 * torch.randn(n, device=dev)) + 0.1j * torch.randn(n, device=dev)
-    ga = torch.zeros(n, dtype=torch.complex64, device=dev)
-    gd = torch.zeros_like(ga)
-    y, dx = torch.empty_like(x), torch.empty_like(x)
+    """Complex AFDF N=8192, 65536 rows in total, sharded over the ranks
+    (AfdfLayer under DataParallel, layers.py:159-215)."""
+    from paper_1511_05946_b200 import AfdfLayer
+    from paper_1511_05946_b200.parallel import DataParallel, shard_rows
+
+    world, rank = _dist()
+    n, total = 8192, args.c5_rows
+    lo, hi = shard_rows(total, world, rank)
+    B = hi - lo
+    g = torch.Generator(device=dev)
+    g.manual_seed(200 + rank)
+    x = torch.randn(B, n, dtype=torch.complex64, device=dev, generator=g)
+    dy = torch.randn(B, n, dtype=torch.complex64, device=dev, generator=g)
+    layer = AfdfLayer(n, device=dev)
+    g.manual_seed(7)
+    layer.a.copy_((1 + 0.1 * torch.randn(n, device=dev, generator=g)) + 0.1j * torch.randn(n, device=dev, generator=g))
+    layer.d.copy_((1 + 0.1 * torch.randn(n, device=dev, generator=g)) + 0.1j * torch.randn(n, device=dev, generator=g))
+    dp = DataParallel(layer)
 
     def step():
-        F.afdf_forward(x, a, d, out=y)
-        F.afdf_backward(x, dy, a.to(torch.complex64), d.to(torch.complex64), ga, gd, accumulate=False, out=dx)
+        dp.zero_grads()
+        dp.forward(x)
+        dp.backward(dy)
+        dp.allreduce_grads()
 
-    ms = timeit(step, args.steps)
-    rps = B / (ms / 1e3)
-    return {"config": "C5 AFDF N=8192 complex64, 8192 rows per GPU (65536 over 8)", "ms_per_step": ms,
-            "rows_per_s_per_gpu": rps, "bytes_per_row": 40 * n,
-            "hbm_roofline_frac": rps * 40 * n / (peak_hbm() * 1e9)}
+    ms = timeit_dist(step, args.steps)
+    rps = total / (ms / 1e3)
+    return {"config": f"C5 AFDF N=8192 complex64, {total} rows over {world} GPU(s)", "n_gpus": world,
+            "rows_per_gpu": B, "ms_per_step": ms, "rows_per_s": rps, "rows_per_s_per_gpu": rps / world,
+            "bytes_per_row": 40 * n, "hbm_roofline_frac_per_gpu": rps / world * 40 * n / (peak_hbm() * 1e9),
+            "scaling": "strong"}
+
+
+MULTI_GPU = ("c4", "c5")
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="c1,sweep,c3,c4,c5")
     ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--bucket-kib", type=int, default=384, help="C4 all-reduce bucket size (8 layers at N=4096)")
+    ap.add_argument("--c5-rows", type=int, default=65536)
     args = ap.parse_args()
-    dev = torch.device("cuda", 0)
-    torch.cuda.set_device(dev)
+    from bench import dist_setup, maybe_spawn
+
+    maybe_spawn(args.gpus, __file__)
+    world, rank, local = dist_setup(args.gpus)
+    dev = torch.device("cuda", local)
     for name in args.only.split(","):
+        if world > 1 and name not in MULTI_GPU:
+            continue  # single-GPU configs
         res = globals()[name](args, dev)
-        for r in (res if isinstance(res, list) else [res]):
-            print(json.dumps(r), flush=True)
+        if rank == 0:
+            for r in (res if isinstance(res, list) else [res]):
+                print(json.dumps(r), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

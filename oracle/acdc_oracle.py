@@ -57,6 +57,8 @@ __all__ = [
     "sgd_step",
     "fp32_tolerance",
     "grad_tolerance",
+    "block_gain",
+    "chain_factor",
 ]
 
 
@@ -347,3 +349,25 @@ def grad_tolerance(n: int, rows: int, ref: np.ndarray) -> float:
     lg = max(1.0, math.log2(max(n, 2))) + max(1.0, math.log2(max(rows, 2)))
     mx = float(np.max(np.abs(ref))) if ref.size else 0.0
     return 4.0 * lg * EPS32 * max(mx, 1.0)
+
+
+def block_gain(a, d) -> float:
+    """rms gain of one ACDC block on an error vector e (layers.py:141-146):
+    C is orthonormal, so ||C3(d * C2(a * e))||_2 = ||d * C2(a * e)||_2, which
+    for rounding errors uncorrelated with the diagonals is rms(a) * rms(d) *
+    ||e||_2.  ReLU (1-Lipschitz) and permutations (isometries) add no gain."""
+    a, d = np.asarray(a), np.asarray(d)
+    return float(np.sqrt(np.mean(np.abs(a) ** 2) * np.mean(np.abs(d) ** 2)))
+
+
+def chain_factor(gains) -> float:
+    """Error bound multiplier for a chain of K blocks, each adding at most the
+    single-layer rounding bound and passing the incoming error on through its
+    gain: sum_{l<K} prod_{l<k<K} g_k (gains in propagation order).  For a
+    cascade's y this is applied to fp32_tolerance (the per-block bound); for dx
+    with the backward's order of gains."""
+    total, prod = 0.0, 1.0
+    for g in reversed(list(gains)):
+        total += prod
+        prod *= g
+    return total

@@ -122,3 +122,45 @@ def fwd_bwd_threaded(layer: RefAcdc, x: np.ndarray, dy: np.ndarray, threads: int
     gd = sum(p[3] for p in parts)
     gb = sum(p[4] for p in parts)
     return y, dx, ga, gd, gb
+
+
+def ref_fft_rows(z: np.ndarray, inverse: bool, threads: int) -> np.ndarray:
+    """Row-wise complex DFT by the reference's compiled ``fft_inplace``
+    (``_kernels.pyx:49-57``; inverse scaled by 1/N, ``transforms.py:174-179``),
+    rows sharded over ``threads`` host threads."""
+    k = load()
+    if k is None:
+        raise RuntimeError("oracle/_ref is not built")
+    z = np.array(z, dtype=np.complex128, order="C", copy=True)
+    n = z.shape[1]
+    t = tables(n)
+    bounds = np.linspace(0, z.shape[0], threads + 1).astype(int)
+
+    def work(i):
+        lo, hi = bounds[i], bounds[i + 1]
+        if hi > lo:
+            k.fft_inplace(z[lo:hi], t.rev, t.tw, bool(inverse))
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(work, range(threads)))
+    return z
+
+
+def afdf_fwd_bwd_threaded(x, dy, a, d, threads: int):
+    """AFDF forward + backward (layers.py:199-215) with the reference's
+    compiled FFT: returns y, dx, grad_a, grad_d (dL/dRe + i dL/dIm)."""
+    n = x.shape[1]
+    h2 = ref_fft_rows(x * a, False, threads)
+    y = ref_fft_rows(h2 * d, True, threads)
+    g3 = ref_fft_rows(dy, False, threads) / n
+    gd = (g3 * np.conj(h2)).sum(axis=0)
+    g1 = ref_fft_rows(g3 * np.conj(d), True, threads) * n
+    ga = (g1 * np.conj(x)).sum(axis=0)
+    return y, g1 * np.conj(a), ga, gd
+
+
+def threads_available() -> int:
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except Exception:  # pragma: no cover
+        return os.cpu_count() or 1

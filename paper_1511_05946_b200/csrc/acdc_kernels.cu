@@ -1086,8 +1086,11 @@ template <bool SGD>
 __global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __restrict__ ws, int64_t groups, int n,
                                                                float* ga, float* gd, float* gb, int accumulate,
                                                                SgdDev sgd) {
-  pdl_launch_dependents();  // e.g. the next cascade block's backward: its prologue overlaps this
-  pdl_wait();               // the backward's partials
+  // e.g. the next cascade block's backward: its prologue overlaps this.  With
+  // the SGD epilogue the trigger waits for the parameter writes (below): a
+  // dependent backward stages a / d into shared memory before its pdl_wait.
+  if constexpr (!SGD) pdl_launch_dependents();
+  pdl_wait();  // the backward's partials
   __shared__ double part[8][33];
   const int o = threadIdx.x & 31, s = threadIdx.x >> 5;
   const int64_t total = 3LL * n;
@@ -1130,6 +1133,10 @@ __global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __re
     } else {
       out[i] = (float)t;
     }
+  }
+  if constexpr (SGD) {  // publish the updated parameters, then let the dependent start
+    __threadfence();
+    pdl_launch_dependents();
   }
 }
 

@@ -221,10 +221,10 @@ int cascade_fwd_f32(const float* x, float* y, int32_t depth, int32_t n, const fl
   int logn;
   int rc = check_n(n, &logn);
   if (rc) return rc;
-  if (cascade_ckpt_bytes(rows, n, depth) == 0)
+  if (cascade_ckpt_bytes(rows > 0 ? rows : 1, n, depth) == 0)
     return set_error(ACDC_E_SIZE, "the fused cascade needs 256 <= n <= 16384 and depth >= 1");
+  if (rows == 0) return ACDC_OK;  // empty batch: nothing to read or write
   if (ldx < n || ldy < n) return ACDC_E_SHAPE;
-  if (rows == 0) return ACDC_OK;
   if (!x || !y || !a || !d || !bias || !ckpt) return ACDC_E_NULL;
   if ((((uintptr_t)x | (uintptr_t)y | (uintptr_t)a) & 7) || (ldx & 1) || (ldy & 1)) return ACDC_E_ALIGN;
   Tables tb;

@@ -74,6 +74,30 @@ def _ld(x: torch.Tensor, n: int) -> int:
     return x.stride(0) if x.shape[0] > 1 else n
 
 
+def _check_out(out: torch.Tensor, like: torch.Tensor, name: str = "out", host_ok: bool = False) -> torch.Tensor:
+    """A caller-supplied output must match ``like``: shape, dtype, rows with
+    unit stride and a row stride the kernels can use, and (unless it is a
+    pinned host buffer the kernels store to directly) the input's device."""
+    if not isinstance(out, torch.Tensor) or out.shape != like.shape or out.dtype != like.dtype:
+        raise ValueError(f"{name} must be a {like.dtype} tensor of shape {tuple(like.shape)}")
+    if out.dim() == 2 and out.shape[0] > 0 and (out.stride(1) != 1 or (out.shape[0] > 1 and out.stride(0) < out.shape[1])):
+        raise ValueError(f"{name} rows must be contiguous with row stride >= {out.shape[1]}")
+    if out.device != like.device and not (host_ok and out.device.type == "cpu" and out.is_pinned()):
+        raise ValueError(f"{name} must be on {like.device}")
+    return out
+
+
+def _check_h2cache(h2cache: torch.Tensor, rows: int, n: int, dev) -> torch.Tensor:
+    need = _lib.load().acdc_h2cache_bytes(rows, n)
+    if need == 0:
+        raise ValueError(f"the h2 cache needs 256 <= n <= 16384, got {n}")
+    if (not isinstance(h2cache, torch.Tensor) or h2cache.device != dev or h2cache.dtype != torch.float32
+            or not h2cache.is_contiguous() or h2cache.numel() * 4 < need):
+        raise ValueError(f"h2cache must be a contiguous fp32 tensor on {dev} of at least {need} bytes "
+                         f"(new_h2cache({rows}, {n}))")
+    return h2cache
+
+
 def prepare(n: int, device=None) -> None:
     """Build tables and launch configuration for size n (call before graph capture)."""
     with torch.cuda.device(device if device is not None else torch.cuda.current_device()):
@@ -104,7 +128,9 @@ def acdc_forward(x: torch.Tensor, a: torch.Tensor, d: torch.Tensor, bias: torch.
     x = _rows2d(x, n)
     dev = x.device
     a, d, bias = (_vec(v, n, dev, nm) for v, nm in ((a, "a"), (d, "d"), (bias, "bias")))
-    y = torch.empty_like(x, memory_format=torch.contiguous_format) if out is None else out
+    y = torch.empty_like(x, memory_format=torch.contiguous_format) if out is None else _check_out(out, x, host_ok=True)
+    if h2cache is not None:
+        _check_h2cache(h2cache, x.shape[0], n, dev)
     lib = _lib.load()
     with torch.cuda.device(dev):
         if h2cache is None:
@@ -145,7 +171,9 @@ def acdc_backward(
     for g in (grad_a, grad_d, grad_bias):
         if g.device != dev or g.dtype != torch.float32 or not g.is_contiguous() or g.shape != (n,):
             raise ValueError("gradient buffers must be contiguous fp32 (n,) tensors on the input device")
-    dx = torch.empty_like(x, memory_format=torch.contiguous_format) if out is None else out
+    dx = torch.empty_like(x, memory_format=torch.contiguous_format) if out is None else _check_out(out, x, host_ok=True)
+    if h2cache is not None:
+        _check_h2cache(h2cache, x.shape[0], n, dev)
     lib = _lib.load()
     with torch.cuda.device(dev):
         wsb = lib.acdc_bwd_workspace_bytes(x.shape[0], n)
@@ -186,7 +214,9 @@ def acdc_backward_sgd(x, dy, params, velocities, lr, weight_decay, momentum, gra
             raise ValueError("parameter, velocity and gradient buffers must be contiguous fp32 (n,) tensors")
     if accumulate and grads is None:
         raise ValueError("accumulate=True needs the gradient buffers")
-    dx = torch.empty_like(x, memory_format=torch.contiguous_format) if out is None else out
+    dx = torch.empty_like(x, memory_format=torch.contiguous_format) if out is None else _check_out(out, x)
+    if h2cache is not None:
+        _check_h2cache(h2cache, x.shape[0], n, dev)
     st = _lib.SgdStep()
     for k in range(3):
         st.value[k] = params[k].data_ptr()
@@ -264,24 +294,32 @@ def ifft(z: torch.Tensor) -> torch.Tensor:
 
 
 class AcdcFunction(torch.autograd.Function):
-    """Autograd wrapper: forward = acdc_fwd_f32, backward = acdc_bwd_f32 with h2
-    recomputed; parameter grads are returned (accumulate=False)
-    and summed into ``.grad`` by autograd."""
+    """Autograd wrapper: forward = acdc_fwd_cache_f32, which also keeps
+    h2 = C2(a*x) like the reference's cache (layers.py:145), and backward =
+    acdc_bwd_cached_f32 (the TMEM backward at 512 <= N <= 8192); sizes without
+    an h2 cache recompute it (acdc_bwd_f32).  Parameter grads
+    are returned (accumulate=False) and summed into ``.grad`` by autograd."""
 
     @staticmethod
     def forward(ctx, x, a, d, bias):
-        y = acdc_forward(x, a, d, bias)
-        ctx.save_for_backward(x, a, d)
+        n = a.shape[0]
+        rows = x.shape[0] if x.dim() == 2 else 0
+        hc = new_h2cache(rows, n, x.device) if (rows > 0 and h2cache_supported(n)) else None
+        y = acdc_forward(x, a, d, bias, h2cache=hc)
+        if hc is None:
+            ctx.save_for_backward(x, a, d)
+        else:
+            ctx.save_for_backward(x, a, d, hc)
         return y
 
     @staticmethod
     def backward(ctx, gy):
-        x, a, d = ctx.saved_tensors
+        x, a, d, *hc = ctx.saved_tensors
         n = a.shape[0]
         ga = torch.empty(n, dtype=torch.float32, device=x.device)
         gd = torch.empty_like(ga)
         gb = torch.empty_like(ga)
-        dx = acdc_backward(x, gy, a, d, ga, gd, gb, accumulate=False)
+        dx = acdc_backward(x, gy, a, d, ga, gd, gb, accumulate=False, h2cache=hc[0] if hc else None)
         return dx, ga, gd, gb
 
 
@@ -314,7 +352,7 @@ def afdf_forward(x: torch.Tensor, a: torch.Tensor, d: torch.Tensor, out=None) ->
     n = a.shape[0]
     x = _crows2d(x, n)
     a, d = _cvec(a, n, x.device, "a"), _cvec(d, n, x.device, "d")
-    y = torch.empty_like(x) if out is None else out
+    y = torch.empty_like(x) if out is None else _check_out(out, x)
     lib = _lib.load()
     with torch.cuda.device(x.device):
         _lib.check(lib.afdf_fwd_c64(_ptr(x), _ptr(y), _ptr(a), _ptr(d), x.shape[0], n, n, n, _stream(x)))
@@ -334,7 +372,7 @@ def afdf_backward(x, dy, a, d, grad_a, grad_d, accumulate: bool = True, out=None
     for g in (grad_a, grad_d):
         if g.device != dev or g.dtype != torch.complex64 or not g.is_contiguous() or g.shape != (n,):
             raise ValueError("gradient buffers must be contiguous complex64 (n,) tensors on the input device")
-    dx = torch.empty_like(x) if out is None else out
+    dx = torch.empty_like(x) if out is None else _check_out(out, x)
     lib = _lib.load()
     with torch.cuda.device(dev):
         wsb = lib.afdf_bwd_workspace_bytes(x.shape[0], n)
@@ -395,11 +433,13 @@ def cascade_forward(x: torch.Tensor, a: torch.Tensor, d: torch.Tensor, bias: tor
     dev = x.device
     a, d, bias = (v.to(device=dev, dtype=torch.float32).contiguous() for v in (a, d, bias))
     lib = _lib.load()
-    nbytes = lib.cascade_ckpt_bytes(x.shape[0], n, depth)
-    if nbytes == 0:
+    if lib.cascade_ckpt_bytes(max(x.shape[0], 1), n, depth) == 0:
         raise ValueError(f"the fused cascade needs 256 <= n <= 16384, got {n}")
+    nbytes = lib.cascade_ckpt_bytes(x.shape[0], n, depth)  # 0 for an empty batch
     ckpt = torch.empty(nbytes // 4, dtype=torch.float32, device=dev)
-    y = torch.empty_like(x, memory_format=torch.contiguous_format) if out is None else out
+    y = torch.empty_like(x, memory_format=torch.contiguous_format) if out is None else _check_out(out, x)
+    if x.shape[0] == 0:
+        return y, ckpt
     with torch.cuda.device(dev):
         _lib.check(lib.cascade_fwd_f32(_ptr(x), _ptr(y), depth, n, _ptr(a), _ptr(d), _ptr(bias), _ptr(perm),
                                        _ptr(flags), _ptr(ckpt), x.shape[0], _ld(x, n), _ld(y, n), _stream(x)))
@@ -415,7 +455,7 @@ def _ckpt_views(ckpt: torch.Tensor, rows: int, n: int, depth: int):
 
 
 def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor | None, flags,
-                     ckpt: torch.Tensor, grads, accumulate: bool = True, sgd=None) -> torch.Tensor:
+                     ckpt: torch.Tensor, grads, accumulate: bool = True, sgd=None, on_block=None) -> torch.Tensor:
     """Backward of :func:`cascade_forward` (layers.py:341-344): one cached-h2
     block backward per block, last to first, each applying the previous block's
     ReLU mask and inverse permutation in its epilogue.  ``a``, ``d``: sequences
@@ -423,13 +463,27 @@ def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor
     fp32 (n,) tensors, accumulated in place; ``flags``: host list of ints.
     ``sgd``: optional per-block (params, velocities, lr3, wd3, momentum): each
     block's momentum-SGD step is fused into its gradient reduction
-    (:func:`acdc_backward_sgd`); the grads are then added in and zeroed."""
+    (:func:`acdc_backward_sgd`); the grads are then added in and zeroed.
+    ``on_block(l)`` is called after block l's kernels are enqueued (e.g. to
+    start that block's gradient all-reduce while earlier blocks run)."""
     depth = len(a)
     n = a[0].shape[0]
     x = _rows2d(x, n)
     g = _rows2d(dy, n, "grad_y")
     rows = x.shape[0]
+    if g.shape[0] != rows:
+        raise ValueError(f"grad_y has {g.shape[0]} rows, forward input had {rows}")
     dev = x.device
+    if rows == 0:  # empty batch: gradients unchanged (+= 0), or zeroed without accumulate
+        if not accumulate:
+            for gr in grads:
+                for t in gr:
+                    t.zero_()
+        if sgd is not None:
+            for l in range(depth - 1, -1, -1):
+                prm, vel, lr3, wd3, mu = sgd[l]
+                acdc_backward_sgd(x, g, prm, vel, lr3, wd3, mu, grads=grads[l], accumulate=accumulate)
+        return torch.empty_like(g)
     xs, h2 = _ckpt_views(ckpt, rows, n, depth)
     fl = [int(f) for f in flags]
     lib = _lib.load()
@@ -447,6 +501,8 @@ def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor
                 acdc_backward_sgd(xl, g, prm, vel, lr3, wd3, mu, grads=(ga, gd, gb), accumulate=accumulate, out=out,
                                   h2cache=h2[l], prev_perm=pp, prev_relu=bool(prev & 1), ws=ws)
                 g = out
+                if on_block is not None:
+                    on_block(l)
                 continue
             al, dl = _vec(a[l], n, dev, "a"), _vec(d[l], n, dev, "d")
             _lib.check(lib.cascade_bwd_block_f32(
@@ -454,6 +510,8 @@ def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor
                 _ptr(ga), _ptr(gd), _ptr(gb), 1 if accumulate else 0, _ptr(ws), wsb, rows, n, _ld(xl, n), _ld(g, n),
                 n, _stream(x)))
             g = out
+            if on_block is not None:
+                on_block(l)
     return g
 
 

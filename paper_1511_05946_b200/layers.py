@@ -448,9 +448,11 @@ class Cascade:
             x = layer.forward(x)
         return Layer._out(x, host)
 
-    def backward(self, grad_y, retain_cache=False, sgd=None):
+    def backward(self, grad_y, retain_cache=False, sgd=None, on_layer=None):
         """``sgd`` (fused stacks only, from ``training.Sgd.backward_step``): per
-        block SGD specs; each block's optimizer step runs in its backward."""
+        block SGD specs; each block's optimizer step runs in its backward.
+        ``on_layer(layer)`` is called once each layer's backward is enqueued
+        (last layer first; in a fused stack for each ACDC layer of a block)."""
         host = not (isinstance(grad_y, torch.Tensor) and grad_y.is_cuda)
         if sgd is not None and self._fused is None:
             raise ValueError("a fused SGD backward needs a fused cascade")
@@ -463,14 +465,18 @@ class Cascade:
             gy, _ = self.layers[-1]._check_input(grad_y)
             fz = self._fused
             acdc = [b[0] for b in fz["blocks"]]
+            hook = (lambda l: on_layer(acdc[l])) if on_layer is not None else None
             dx = F.cascade_backward(xt, gy, [l.a for l in acdc], [l.d for l in acdc], fz["perm"], fz["flags"], ckpt,
-                                    [(l.grad_a, l.grad_d, l.grad_bias_d) for l in acdc], accumulate=True, sgd=sgd)
+                                    [(l.grad_a, l.grad_d, l.grad_bias_d) for l in acdc], accumulate=True, sgd=sgd,
+                                    on_block=hook)
             return Layer._out(dx, host)
         g = grad_y
         if host:
             g, _ = self.layers[-1]._check_input(grad_y, torch.complex64 if self.complex_domain else torch.float32)
         for layer in reversed(self.layers):
             g = layer.backward(g, retain_cache=retain_cache)
+            if on_layer is not None:
+                on_layer(layer)
         return Layer._out(g, host)
 
     def params(self):

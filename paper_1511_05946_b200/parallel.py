@@ -69,9 +69,15 @@ class DataParallel:
     rank's rows; ``allreduce_grads()`` sums the gradients over ranks (one
     collective, optionally async).  The wrapped layers' ``grad_*`` attributes
     are rebound to views of the flat buffer.
+
+    ``bucket_bytes`` (cascades): the flat buffer is cut into
+    buckets of whole layers, in backward order; a bucket's all-reduce is
+    started (async) as soon as its last layer's backward is enqueued, so it
+    overlaps the backward of the earlier layers, and ``allreduce_grads()``
+    only waits for the outstanding buckets.  Same sums as one collective.
     """
 
-    def __init__(self, model, group=None):
+    def __init__(self, model, group=None, bucket_bytes: int | None = None):
         self.model = model
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -79,15 +85,23 @@ class DataParallel:
         layers = model.layers if hasattr(model, "layers") else [model]
         # every parameter including fixed ones (fix_a AFDF still computes grad_a)
         self._params = []
+        spans, off = {}, 0
         for layer in layers:
             ps = getattr(layer, "_params", None) or layer.params()
             self._params.extend(ps)
+            sz = sum(_real_view(p.grad).numel() for p in ps)
+            spans[id(layer)] = (off, off + sz)
+            off += sz
         self.flat = flatten_grads(self._params)
         for layer in layers:  # keep layer attributes pointing at the live views
             for p in getattr(layer, "_params", []) or []:
                 attr = "grad_" + p.name
                 if hasattr(layer, attr):
                     setattr(layer, attr, p.grad)
+        self._spans = spans
+        self.bucket_bytes = bucket_bytes
+        self._pending = None  # [lo, hi) of flat not yet handed to a collective
+        self._works = []
 
     def shard(self, rows: int) -> tuple[int, int]:
         return shard_rows(rows, self.world, self.rank)
@@ -95,15 +109,48 @@ class DataParallel:
     def forward(self, x):
         return self.model.forward(x)
 
-    def backward(self, grad_y, retain_cache=False):
-        return self.model.backward(grad_y, retain_cache=retain_cache)
+    def _on_layer(self, layer):
+        span = self._spans.get(id(layer))
+        if span is None or span[0] == span[1]:
+            return
+        lo, hi = span
+        if self._pending is None:
+            self._pending = [lo, hi]
+        else:  # backward order: each layer sits just below the pending span
+            self._pending[0] = min(self._pending[0], lo)
+            self._pending[1] = max(self._pending[1], hi)
+        if (self._pending[1] - self._pending[0]) * 4 >= self.bucket_bytes or self._pending[0] == 0:
+            self._flush()
+
+    def _flush(self):
+        lo, hi = self._pending
+        self._pending = None
+        self._works.append(dist.all_reduce(self.flat[lo:hi], op=dist.ReduceOp.SUM, group=self.group, async_op=True))
+
+    def backward(self, grad_y, retain_cache=False, **kw):
+        if self.world > 1 and self.bucket_bytes and hasattr(self.model, "layers"):
+            self._works, self._pending = [], None
+            out = self.model.backward(grad_y, retain_cache=retain_cache, on_layer=self._on_layer, **kw)
+            if self._pending is not None:
+                self._flush()
+            return out
+        return self.model.backward(grad_y, retain_cache=retain_cache, **kw)
 
     def zero_grads(self):
         self.flat.zero_()
 
     def allreduce_grads(self, async_op: bool = False):
-        """Sum gradients over ranks (NCCL over NVLink on GPUs, gloo on CPU)."""
+        """Sum gradients over ranks (NCCL over NVLink on GPUs, gloo on CPU).
+        With buckets already in flight from :meth:`backward`, waits for them
+        (the caller's stream then follows the collectives)."""
         if self.world == 1:
+            return None
+        if self._works:
+            works, self._works = self._works, []
+            if async_op:
+                return works
+            for w in works:
+                w.wait()
             return None
         return dist.all_reduce(self.flat, op=dist.ReduceOp.SUM, group=self.group, async_op=async_op)
 

@@ -60,6 +60,16 @@ class _FakeCascade:
     def params(self):
         return [p for l in self.layers for p in l.params()]
 
+    def backward(self, grads, retain_cache=False, on_layer=None):
+        """Add precomputed per-layer grads last layer first, calling
+        ``on_layer`` after each (the Cascade.backward hook protocol)."""
+        for l, (ga, gd, gb) in reversed(list(zip(self.layers, grads))):
+            l.grad_a += torch.tensor(ga, dtype=torch.float32)
+            l.grad_d += torch.tensor(gd, dtype=torch.float32)
+            l.grad_bias_d += torch.tensor(gb, dtype=torch.float32)
+            if on_layer is not None:
+                on_layer(l)
+
 
 def _free_port():
     s = socket.socket()
@@ -69,7 +79,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, n, rows, depth, q):
+def _worker(rank, world, port, n, rows, depth, q, bucket=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -80,17 +90,17 @@ def _worker(rank, world, port, n, rows, depth, q):
         layers = [_FakeAcdc(n, rng) for _ in range(depth)]
         x = rng.standard_normal((rows, n))
         dy = rng.standard_normal((rows, n))
-        dp = DataParallel(_FakeCascade(layers))
+        dp = DataParallel(_FakeCascade(layers), bucket_bytes=bucket)
         lo, hi = dp.shard(rows)
         # local forward/backward through the stack with the oracle (scaffolding)
         specs = [{"kind": "acdc", "a": l.a.numpy(), "d": l.d.numpy(), "bias": l.bias_d.numpy()} for l in layers]
         _, caches = O.cascade_forward(x[lo:hi], specs)
         _, grads = O.cascade_backward(dy[lo:hi], specs, caches)
-        for l, (ga, gd, gb) in zip(layers, grads):
-            l.grad_a += torch.tensor(ga, dtype=torch.float32)
-            l.grad_d += torch.tensor(gd, dtype=torch.float32)
-            l.grad_bias_d += torch.tensor(gb, dtype=torch.float32)
+        dp.backward(grads)  # bucketed: all-reduces start inside, last layers first
+        nbuckets = len(dp._works)
         dp.allreduce_grads()
+        if bucket:  # 3 layers x 3n fp32 = 192 B each; 100-byte buckets: one per layer
+            assert nbuckets == depth, nbuckets
         # full-batch reference on every rank
         _, caches = O.cascade_forward(x, specs)
         _, full = O.cascade_backward(dy, specs, caches)
@@ -103,13 +113,13 @@ def _worker(rank, world, port, n, rows, depth, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_dp_allreduce_equals_full_batch(world):
+@pytest.mark.parametrize("world,bucket", [(2, None), (3, None), (2, 100)])
+def test_dp_allreduce_equals_full_batch(world, bucket):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
     n, rows, depth = 16, 11, 3
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, rows, depth, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, rows, depth, q, bucket)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(world)]

@@ -183,3 +183,24 @@ def test_sgd_matches_reference_update():
     for p, r in zip(ps, ref_p):
         np.testing.assert_allclose(p.value.numpy(), r, atol=1e-12)
         assert float(p.grad.abs().sum()) == 0.0
+
+
+def test_ref_afdf_and_chain_tolerance():
+    """The reference-compiled AFDF driver (used by the full-shape GPU tests)
+    agrees with the numpy restatement; chain_factor sums gain products."""
+    from oracle import ref_kernels
+
+    if ref_kernels.load() is None:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(3)
+    n, rows = 64, 9
+    c = lambda *s: rng.standard_normal(s) + 1j * rng.standard_normal(s)
+    x, dy, a, d = c(rows, n), c(rows, n), 1 + 0.1 * c(n), 1 + 0.1 * c(n)
+    y, dx, ga, gd = ref_kernels.afdf_fwd_bwd_threaded(x, dy, a, d, threads=2)
+    yr, h2 = O.afdf_forward(x, a, d)
+    dxr, gar, gdr = O.afdf_backward(x, h2, dy, a, d)
+    for m, r in ((y, yr), (dx, dxr), (ga, gar), (gd, gdr)):
+        assert np.abs(m - r).max() < 1e-9 * max(1.0, np.abs(r).max())
+    assert O.chain_factor([1.0] * 5) == 5.0
+    assert abs(O.chain_factor([2.0, 2.0, 2.0]) - 7.0) < 1e-12  # 1 + 2 + 4
+    assert abs(O.block_gain(np.ones(8), 2 * np.ones(8)) - 2.0) < 1e-12

@@ -196,10 +196,10 @@ def test_layer_api_matches_reference_contract(golden):
         AcdcLayer(100)
 
 
-def test_autograd_function():
+@pytest.mark.parametrize("n,rows", [(128, 9), (512, 37), (4096, 64)])  # recompute / h2 cache / TMEM backward
+def test_autograd_function(n, rows):
     from paper_1511_05946_b200 import acdc
 
-    n, rows = 512, 37
     rng = np.random.default_rng(11)
     x = t32(f32(rng, rows, n)).requires_grad_()
     a = t32(f32(rng, n, mean=1, std=0.3)).requires_grad_()
