@@ -1,0 +1,77 @@
+"""One small call of every kernel family, for compute-sanitizer
+(memcheck / racecheck / synccheck / initcheck).
+
+Covers: forward (recompute and h2-cache) + TMEM backward (mbarrier bulk copies
+of dy into the reused exchange buffer, TMEM alloc/dealloc, cross-group
+parking) launched back to back under PDL, the recompute backward, the
+two-stage gradient reduction (many row groups at N=128), the SGD-fused
+reduction followed by a dependent backward, the fused cascade forward and
+its block backwards (ReLU / inverse-perm epilogues, PDL chain), AFDF forward
+and backward, the complex FFT and the DCT / IDCT kernels.
+usage: python scripts/sanitize_probe.py
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1511_05946_b200 import AcdcLayer, Cascade, PermutationLayer, ReluLayer  # noqa: E402
+from paper_1511_05946_b200 import functional as F  # noqa: E402
+
+dev = torch.device("cuda", 0)
+g = torch.Generator(device=dev)
+g.manual_seed(0)
+rn = lambda *s: torch.randn(*s, device=dev, generator=g)
+
+
+def layer(n, rows, cache):
+    x, dy = rn(rows, n), rn(rows, n)
+    a, d, b = 1 + 0.1 * rn(n), 1 + 0.1 * rn(n), 0.1 * rn(n)
+    gr = torch.zeros(3, n, device=dev)
+    hc = F.new_h2cache(rows, n, dev) if cache else None
+    for _ in range(2):  # back to back: PDL forward -> backward -> reduction -> next forward
+        y = F.acdc_forward(x, a, d, b, h2cache=hc)
+        F.acdc_backward(x, y if cache else dy, a, d, gr[0], gr[1], gr[2], h2cache=hc)
+
+
+layer(1024, 12, True)     # TMEM backward (2 groups per CTA), odd row pairs per group
+layer(4096, 7, True)      # TMEM backward at the metric size, a ragged last pair
+layer(4096, 6, False)     # recompute backward
+layer(128, 2100, False)   # two-stage reduction (many row groups)
+layer(16384, 3, True)     # legacy cached backward, tables in global memory
+# SGD-fused reduction, then a backward of the same layer (PDL ordering)
+n, rows = 1024, 10
+x, dy = rn(rows, n), rn(rows, n)
+a, d, b = 1 + 0.1 * rn(n), 1 + 0.1 * rn(n), torch.zeros(n, device=dev)
+vel = [torch.zeros(n, device=dev) for _ in range(3)]
+hc = F.new_h2cache(rows, n, dev)
+F.acdc_forward(x, a, d, b, h2cache=hc)
+for _ in range(2):
+    F.acdc_backward_sgd(x, dy, (a, d, b), vel, (0.1,) * 3, (0.0,) * 3, 0.9, h2cache=hc)
+# fused cascade (ReLU + Perm epilogues)
+rng = np.random.default_rng(0)
+ls = []
+for i in range(3):
+    L = AcdcLayer(512, device=dev)
+    L.a.normal_(1.0, 0.1)
+    ls.append(L)
+    if i < 2:
+        ls += [ReluLayer(512, device=dev), PermutationLayer(512, perm=rng.permutation(512), device=dev)]
+c = Cascade(ls)
+c.forward(rn(9, 512))
+c.backward(rn(9, 512))
+# AFDF, FFT, DCT
+for n in (256, 8192):
+    z = torch.complex(rn(5, n), rn(5, n))
+    a = torch.complex(1 + 0.1 * rn(n), 0.1 * rn(n))
+    ga, gd = torch.zeros(n, dtype=torch.complex64, device=dev), torch.zeros(n, dtype=torch.complex64, device=dev)
+    y = F.afdf_forward(z, a, a)
+    F.afdf_backward(z, y, a, a, ga, gd)
+    F.fft(z)
+    F.ifft(z)
+F.dct(rn(3, 4096))
+F.idct(rn(3, 4096))
+torch.cuda.synchronize()
+print("sanitize probe ok")
