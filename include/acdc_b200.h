@@ -91,8 +91,11 @@ int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, con
  * acdc_fwd_cache_f32 also writes h2 into `h2cache` (acdc_h2cache_bytes(rows, n)
  * bytes, opaque layout); acdc_bwd_cached_f32 reads it instead of recomputing
  * C2(a*x), trading 8n bytes/row of HBM traffic for one of the backward's three
- * transforms.  Same results as the pair above.  256 <= n <= 16384 (bytes() == 0
- * otherwise). */
+ * transforms.  Same results as the pair above.  256 <= n <= 32768 (bytes() == 0
+ * otherwise).  For n >= 8192 the kernels run the half-length plan (one
+ * n/2-point complex FFT per row) and need 16-byte aligned rows with ld a
+ * multiple of 4 (ACDC_E_ALIGN otherwise); the cache layout follows the plan,
+ * so a cache is only valid for the backward of the same size. */
 size_t acdc_h2cache_bytes(int64_t rows, int32_t n);
 int acdc_fwd_cache_f32(const float* x, float* y, const float* a, const float* d, const float* bias, float* h2cache,
                        int64_t rows, int32_t n, int64_t ldx, int64_t ldy, acdc_stream_t stream);
@@ -114,7 +117,10 @@ int acdc_bwd_cached_f32(const float* x, const float* dy, float* dx, const float*
  * off (the reference's diagonals).  grad_* may be NULL unless accumulate; if
  * given they are zeroed, like the reference's p.grad[...] = 0.  value[0] and
  * value[1] are the a and d the backward reads (before the update: stream
- * order).  The update is computed in fp64 from the fp32 state. */
+ * order).  The update is computed in fp64 from the fp32 state.
+ * prev_relu: bit 0 = the previous block's ReLU epilogue; bit 1 = h2cache was
+ * written by cascade_fwd_f32 (the cascade's row-pair layout) rather than by
+ * acdc_fwd_cache_f32. */
 typedef struct acdc_sgd_step {
   float* value[3];        /* a, d, bias_d: [n] fp32, updated in place */
   float* velocity[3];     /* momentum buffers: [n] fp32 */

@@ -35,5 +35,6 @@ from .layers import (
     load_cascade,
     save_cascade,
 )
+from .plans import DctPlan, FftPlan, dct_matrix, resolve_backend
 
 __version__ = "0.1.0"

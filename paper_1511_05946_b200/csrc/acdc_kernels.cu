@@ -26,26 +26,9 @@
 #include "tma.cuh"
 #include "tmem.cuh"
 #include "runtime.h"
+#include "kparams.h"
 
 namespace acdc {
-
-struct KParams {
-  const float* x;
-  const float* dy;
-  float* y;  // y (fwd) or dx (bwd)
-  const float* a;
-  const float* d;
-  const float* bias;
-  float* ws;          // bwd partials [groups][3][N]
-  float* scratch;     // bwd stash when it does not fit in smem [groups][STASH*T]
-  float* h2c;         // h2 cache [row pairs][2N] in thread-native layout (H2C kernels)
-  const int* epi_perm;  // bwd epilogue (fused cascade): scatter dx through this permutation
-  int epi_relu;         // bwd epilogue: zero dx where x <= 0 (the previous block's ReLU)
-  int stage;            // bwd (TMEM kernel): dy rows are 16-byte aligned -> bulk-copy them into smem ahead
-  const float2* tab;  // [pass twiddles | c'_k]
-  int64_t rows;
-  int64_t ldx, ldy, ldo;
-};
 
 // ---------------------------------------------------------------- helpers
 
@@ -1224,7 +1207,9 @@ static size_t red_tmp_bytes(int64_t groups, int32_t n) {
 
 // ---------------------------------------------------------------- host side
 
-enum Kind { K_FWD = 0, K_BWD = 1, K_DCT2 = 2, K_DCT3 = 3, K_FWD_H2 = 4, K_BWD_H2 = 5 };
+// K_BWD_H2_RP: cached backward whose h2 cache comes from the fused cascade
+// forward (always the row-pair layout, even at half-length sizes).
+enum Kind { K_FWD = 0, K_BWD = 1, K_DCT2 = 2, K_DCT3 = 3, K_FWD_H2 = 4, K_BWD_H2 = 5, K_BWD_H2_RP = 6 };
 
 template <class K>
 static void geom(LaunchInfo& li, int scratch) {
@@ -1330,11 +1315,34 @@ static int launch_info(int logn, int kind, LaunchInfo* li) {
   }
 }
 
-static int sized(int logn, int kind, int64_t rows, LaunchInfo* li, int64_t* grid) {
-  int rc = launch_info(logn, kind, li);
-  if (rc) return rc;
-  if (!li->fn) return set_error(ACDC_E_SIZE, "the h2 cache needs n >= 256 and n <= 16384");
-  return grid_for(*li, (rows + 1) / 2, grid);
+// Half-length plan (hl_kernels.cu) for the large sizes: rows move as 128-bit
+// quads.  The kinds that touch the h2 cache must pick the same plan in the
+// forward and the backward (the cache layouts differ), so for them the plan
+// depends on the size only and misaligned rows are an error; the other kinds
+// fall back to the row-pair kernels.
+static bool quad_aligned(const void* q, int64_t ld) { return (((uintptr_t)q & 15) == 0) && (ld & 3) == 0; }
+static bool cache_kind(int kind) { return kind == K_FWD_H2 || kind == K_BWD_H2; }
+
+static int sized(int logn, int kind, int64_t rows, LaunchInfo* li, int64_t* grid, bool allow_hl = true) {
+  int rc;
+  if (!(allow_hl && hl_launch_info(logn, kind, li))) {
+    if ((rc = launch_info(logn, kind == K_BWD_H2_RP ? K_BWD_H2 : kind, li))) return rc;
+  }
+  if (!li->fn) return set_error(ACDC_E_SIZE, "the h2 cache needs n >= 256 and n <= 16384 (32768 on the half-length plan)");
+  return grid_for(*li, (rows + li->unit_rows - 1) / li->unit_rows, grid);
+}
+
+// Plan choice for one call (shared by run() and the backward's reduction sizing).
+static int plan_hl(int logn, int kind, const KParams& p, bool* allow) {
+  *allow = true;
+  if (!hl_enabled(logn) || kind == K_BWD_H2_RP || kind == K_DCT2 || kind == K_DCT3) return ACDC_OK;
+  bool ok = quad_aligned(p.x, p.ldx) && quad_aligned(p.y, p.ldo) && (((uintptr_t)p.a & 15) == 0);
+  if (kind == K_BWD || kind == K_BWD_H2) ok = ok && quad_aligned(p.dy, p.ldy);
+  if (ok) return ACDC_OK;
+  if (cache_kind(kind))
+    return set_error(ACDC_E_ALIGN, "at this size the h2-cache kernels need 16-byte aligned rows (ld a multiple of 4)");
+  *allow = false;
+  return ACDC_OK;
 }
 
 // Rows of n >= 256 are moved as 64-bit pairs: pointers 8-byte aligned, even ld.
@@ -1347,12 +1355,14 @@ static int run(int kind, KParams p, int32_t n, cudaStream_t st) {
   int rc = check_n(n, &logn);
   if (rc) return rc;
   if (p.rows == 0) return ACDC_OK;
-  Tables tb;
-  if ((rc = get_tables(logn, &tb))) return rc;
-  p.tab = tb.tab;
+  bool allow;
+  if ((rc = plan_hl(logn, kind, p, &allow))) return rc;
   LaunchInfo li;
   int64_t grid;
-  if ((rc = sized(logn, kind, p.rows, &li, &grid))) return rc;
+  if ((rc = sized(logn, kind, p.rows, &li, &grid, allow))) return rc;
+  Tables tb;
+  if ((rc = li.hl ? get_tables_hl(logn, &tb) : get_tables(logn, &tb))) return rc;
+  p.tab = tb.tab;
   return launch(li, grid, &p, st);
 }
 
@@ -1370,10 +1380,12 @@ int acdc_prepare(int32_t n) {
   if (logn == 0) return ACDC_OK;
   Tables tb;
   if ((rc = get_tables(logn, &tb))) return rc;
+  if (hl_enabled(logn) && (rc = get_tables_hl(logn, &tb))) return rc;
   for (int k = 0; k < 4; ++k) {
     LaunchInfo li;
     int64_t grid;
     if ((rc = sized(logn, k, 2, &li, &grid))) return rc;
+    if (hl_enabled(logn) && (k == K_FWD || k == K_BWD) && (rc = sized(logn, k, 2, &li, &grid, false))) return rc;
   }
   return ACDC_OK;
 }
@@ -1419,8 +1431,9 @@ int acdc_fwd_f32(const float* x, float* y, const float* a, const float* d, const
 }
 
 size_t acdc_h2cache_bytes(int64_t rows, int32_t n) {
-  if (n < 256 || n > 16384 || (n & (n - 1)) != 0 || rows < 0) return 0;
-  return (size_t)((rows + 1) / 2) * 2 * (size_t)n * sizeof(float);
+  if (n < 256 || n > 32768 || (n & (n - 1)) != 0 || rows < 0) return 0;
+  if (n == 32768 && !hl_enabled(15)) return 0;  // the row-pair kernels cache h2 up to 16384
+  return (size_t)((rows + 1) / 2) * 2 * (size_t)n * sizeof(float);  // covers both layouts
 }
 
 int acdc_fwd_cache_f32(const float* x, float* y, const float* a, const float* d, const float* bias, float* h2cache,
@@ -1436,11 +1449,15 @@ size_t acdc_bwd_workspace_bytes(int64_t rows, int32_t n) {
   // large enough for both backward kernels (recompute and h2-cache differ in
   // groups per CTA and stash placement)
   size_t best = 0;
-  for (int kind : {K_BWD, K_BWD_H2}) {
+  for (int kind : {K_BWD, K_BWD_H2, K_BWD_H2_RP})
+  for (int hl = 0; hl < 2; ++hl) {
     LaunchInfo li;
     int64_t grid;
-    if (launch_info(logn, kind, &li) || !li.fn) continue;
-    if (grid_for(li, ((rows > 0 ? rows : 1) + 1) / 2, &grid)) return 0;
+    if (hl ? !hl_launch_info(logn, kind, &li) : (launch_info(logn, kind == K_BWD_H2_RP ? K_BWD_H2 : kind, &li) != 0))
+      continue;
+    if (!li.fn) continue;
+    const int64_t r = rows > 0 ? rows : 1;
+    if (grid_for(li, (r + li.unit_rows - 1) / li.unit_rows, &grid)) return 0;
     const int64_t groups = grid * (li.red_per_cta ? li.red_per_cta : li.gpc);
     const size_t b = (size_t)groups * (3 * (size_t)n + (size_t)li.scratch) * sizeof(float) + red_tmp_bytes(groups, n);
     best = b > best ? b : best;
@@ -1455,7 +1472,7 @@ int acdc_bwd_launch_count(int64_t rows, int32_t n, int cached) {
   if (logn == 0) return 2;
   LaunchInfo li;
   int64_t grid;
-  if (sized(logn, cached ? K_BWD_H2 : K_BWD, rows, &li, &grid)) return -1;
+  if (sized(logn, cached ? K_BWD_H2 : K_BWD, rows, &li, &grid, true)) return -1;  // contiguous rows
   return grid * (li.red_per_cta ? li.red_per_cta : li.gpc) > RED_CHUNK ? 3 : 2;  // backward + one or two reduction kernels
 }
 
@@ -1464,7 +1481,7 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
                     size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, int64_t lddx,
                     acdc_stream_t stream, const int32_t* epi_perm = nullptr, int epi_relu = 0,
                     const SgdDev* sgd = nullptr) {
-  if (kind == K_BWD_H2 && rows > 0 && !h2c) return ACDC_E_NULL;
+  if ((kind == K_BWD_H2 || kind == K_BWD_H2_RP) && rows > 0 && !h2c) return ACDC_E_NULL;
   int rc = check_common(x, dx, rows, n, ldx, lddx);
   if (rc) return rc;
   if (ldy < n) return ACDC_E_SHAPE;
@@ -1515,7 +1532,9 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
   } else {
     LaunchInfo li;
     int64_t grid;
-    if ((rc = sized(logn, kind, rows, &li, &grid))) return rc;
+    bool allow;
+    if ((rc = plan_hl(logn, kind, p, &allow))) return rc;
+    if ((rc = sized(logn, kind, rows, &li, &grid, allow))) return rc;
     groups = grid * (li.red_per_cta ? li.red_per_cta : li.gpc);
     scratch_floats = li.scratch;
     p.scratch = p.ws + groups * 3 * (int64_t)n;  // scratch follows the partials
@@ -1570,8 +1589,8 @@ int cascade_bwd_block_f32(const float* x, const float* dy, float* dx, const floa
                           int64_t ldx, int64_t ldy, int64_t lddx, acdc_stream_t stream) {
   if (acdc_h2cache_bytes(rows, n) == 0) return set_error(ACDC_E_SIZE, "the fused cascade needs 256 <= n <= 16384");
   if (prev_perm && dx == dy) return set_error(ACDC_E_SHAPE, "the permuted epilogue cannot write in place");
-  return bwd_impl(K_BWD_H2, x, dy, dx, a, d, h2cache, grad_a, grad_d, grad_bias, accumulate, ws, ws_bytes, rows, n,
-                  ldx, ldy, lddx, stream, prev_perm, prev_relu);
+  return bwd_impl(K_BWD_H2_RP, x, dy, dx, a, d, h2cache, grad_a, grad_d, grad_bias, accumulate, ws, ws_bytes, rows,
+                  n, ldx, ldy, lddx, stream, prev_perm, prev_relu);
 }
 
 int acdc_bwd_sgd_f32(const float* x, const float* dy, float* dx, const float* h2cache, const int32_t* prev_perm,
@@ -1593,8 +1612,10 @@ int acdc_bwd_sgd_f32(const float* x, const float* dy, float* dx, const float* h2
   if (prev_perm && dx == dy) return set_error(ACDC_E_SHAPE, "the permuted epilogue cannot write in place");
   if (h2cache && acdc_h2cache_bytes(rows, n) == 0)
     return set_error(ACDC_E_SIZE, "the h2 cache needs n >= 256 and n <= 16384");
-  return bwd_impl(h2cache ? K_BWD_H2 : K_BWD, x, dy, dx, step->value[0], step->value[1], h2cache, grad_a, grad_d,
-                  grad_bias, accumulate, ws, ws_bytes, rows, n, ldx, ldy, lddx, stream, prev_perm, prev_relu, &sg);
+  // prev_relu bit 1: the cache is the fused cascade's (row-pair layout)
+  const int kind = !h2cache ? K_BWD : ((prev_relu & 2) || prev_perm ? K_BWD_H2_RP : K_BWD_H2);
+  return bwd_impl(kind, x, dy, dx, step->value[0], step->value[1], h2cache, grad_a, grad_d, grad_bias, accumulate, ws,
+                  ws_bytes, rows, n, ldx, ldy, lddx, stream, prev_perm, prev_relu & 1, &sg);
 }
 
 static int transform(int kind, const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy,

@@ -1,0 +1,478 @@
+// Half-length (HL) plan for long rows: N = 2^13 ... 2^15 (sm_100a).
+//
+// The row-pair kernels (acdc_kernels.cu) put two rows into one N-point
+// complex FFT; at N >= 16384 that group needs 1024 threads with 32 or 64
+// registers each and spills.  Here ONE row is one N/2-point complex FFT of
+//   z[m] = v[2m] + i v[2m+1],   v = x[reorder]   (Makhoul, transforms.py:109-113)
+// so a group is half as large and the engine is the M = N/2 fast-pairing
+// engine of fft_engine.cuh / dct_pair.cuh unchanged.  With the reorder,
+//   z[m] = x[4m] + i x[4m+2],   z[M-1-m] = x[4m+3] + i x[4m+1]   (m < M/2)
+// so one 128-bit load of x[4m..4m+3] feeds a thread's slot and its partner
+// lane's mirror slot (the spatial pairing the engine already shuffles).
+//
+// DCT-II (reference _kernels.pyx:60-73, X_j = Re(w4s_j V_j), V = FFT_N(v)):
+// with Z = FFT_M(z), the frequency pairing k <-> M-k of the engine gives
+//   P = Z_k + conj Z_{M-k},  Q = -i (Z_k - conj Z_{M-k}),  U = W_N^k Q
+//   2 V_k = P + U,   2 V_{M-k} = conj(P - U)
+// and, w4s = 2 c' (c'_j = s_j e^{-i pi j/2N} / 2, the row-pair tables),
+//   X_k = Re(c'_k 2V_k),        X_{N-k} = -Im(c'_k 2V_k)
+//   X_{M-k} = Re(c'_{M-k} 2V_{M-k}),  X_{M+k} = -Im(c'_{M-k} 2V_{M-k}).
+// Each slot owns the four bins {k, N-k, M-k, M+k}; the self-paired slot of
+// thread 0 owns {0, M, M/2, 3M/2}.
+//
+// DCT-III (reference _kernels.pyx:76-91: V'_j = u1_j y_j - i u2_j y_{N-j},
+// out[reorder] = Re IFFT_N(V')): with F_j = V'_j / N = conj(c'_j)(y_j - i y_{N-j}),
+//   A = F_k + conj F_{M-k},  D = F_k - conj F_{M-k}
+//   G_k = conj(A) - i W conj(D),   G_{M-k} = A - i conj(W) D     (W = W_N^k)
+// H = FFT_M(G) (a FORWARD FFT: IFFT(Z') = conj FFT(conj Z') / M, the 1/M and
+// the 1/N folded in), z' = conj H: out[4m] = Re H_m, out[4m+2] = -Im H_m,
+// out[4m+3] = Re H_{M-1-m}, out[4m+1] = -Im H_{M-1-m}.
+//
+// Backward (layers.py:148-156): g3 = DCT-II(dy) per bin, grad_bias += g3,
+// grad_d += h2 g3 (h2 from the forward's cache, same bin layout), g1 =
+// DCT-III(d g3), grad_a += x g1, dx = a g1.  The 96 per-thread gradient
+// accumulators (3 x 4 bins x 8 slots) live in tensor memory; at N = 32768
+// (1024-thread groups, 64 TMEM columns per thread) grad_a goes to the CTA's
+// partial row in global memory instead (read-modify-write, L2-resident).
+#include <cuda_runtime.h>
+
+#include "kernel_common.cuh"
+#include "kparams.h"
+#include "runtime.h"
+#include "tmem.cuh"
+
+namespace acdc {
+
+template <int LOGN>
+struct GeoHL : Geo<LOGN - 1> {
+  using B = Geo<LOGN - 1>;
+  static constexpr int NR = 1 << LOGN;  // row length
+  static constexpr int M = B::N;        // complex FFT length
+  static constexpr int CPH = M + 1;     // c'_j, j <= N/2
+  static constexpr int WNH = M / 2 + 1; // W_N^k, k <= N/4
+  static constexpr int TAB_HL = (2 * (B::TW_ENTRIES + CPH + WNH) + 3) & ~3;  // floats
+  static constexpr int SMEM_LIMIT = 227 * 1024;
+  __host__ __device__ static constexpr int by(bool tab, int nbuf) {
+    return 4 * ((tab ? TAB_HL : 0) + B::GPC * nbuf * B::BUF_FLOATS);
+  }
+  static constexpr bool TW_SMEM = by(true, 1) <= SMEM_LIMIT;
+  static constexpr int NBUF = TW_SMEM ? (by(true, 2) <= SMEM_LIMIT ? 2 : 1) : (by(false, 2) <= SMEM_LIMIT ? 2 : 1);
+  static constexpr int TAB_FLOATS = TW_SMEM ? TAB_HL : 0;
+  static constexpr int GROUP_FLOATS = NBUF * B::BUF_FLOATS;
+  static constexpr int SMEM_BYTES = by(TW_SMEM, NBUF);
+  static_assert(B::FP && !B::SPLIT, "the half-length plan runs on the fast-pairing engine");
+};
+
+template <class G>
+__device__ __forceinline__ void stage_tables_hl(const float2* tab, float* smem, const float2*& tw, const float2*& cp,
+                                                const float2*& wn) {
+  constexpr int TOT = G::TW_ENTRIES + G::CPH + G::WNH;
+  if constexpr (G::TW_SMEM) {
+    float2* st = reinterpret_cast<float2*>(smem);
+    for (int i = threadIdx.x; i < TOT; i += blockDim.x) st[i] = tab[i];
+    __syncthreads();
+    tw = st;
+  } else {
+    tw = tab;
+  }
+  cp = tw + G::TW_ENTRIES;
+  wn = cp + G::CPH;
+}
+
+// Bins of frequency slot s (k = jfq + s*S): {k, N-k, M-k, M+k}; special {0, M, M/2, 3M/2}.
+template <class G>
+struct HlSlot {
+  int b[4];
+  bool sp;
+  __device__ __forceinline__ HlSlot(const FastMap<G>& fm, int s) {
+    sp = fm.special(s);
+    const int k = fm.jfq + s * FastMap<G>::S;
+    b[0] = sp ? 0 : k;
+    b[1] = sp ? G::M : G::NR - k;
+    b[2] = sp ? G::M / 2 : G::M - k;
+    b[3] = sp ? 3 * G::M / 2 : G::M + k;
+  }
+};
+
+// Per-slot table values: cA = c'_{b0}, cB = c'_{b2} (special: c'_M), W = W_N^k (special: c'_{M/2}).
+template <class G>
+__device__ __forceinline__ void hl_coefs(const float2* cp, const float2* wn, const FastMap<G>& fm, int s, float2& cA,
+                                         float2& cB, float2& W) {
+  const int k = fm.jfq + s * FastMap<G>::S;
+  if (fm.special(s)) {
+    cA = tab_load<G>(cp, 0);
+    cB = tab_load<G>(cp, G::M);
+    W = tab_load<G>(cp, G::M / 2);
+  } else {
+    cA = tab_load<G>(cp, k);
+    cB = tab_load<G>(cp, G::M - k);
+    W = tab_load<G>(wn, k);
+  }
+}
+
+__device__ __forceinline__ float2 conj2(float2 z) { return make_float2(z.x, -z.y); }
+
+// DCT-II post-pass of one slot: (Z_k, Z_{M-k}) -> X at the slot's four bins.
+__device__ __forceinline__ float4 hl_post(float2 zl, float2 zh, float2 cA, float2 cB, float2 W, bool special) {
+  if (special) {  // zl = Z_0, zh = Z_{M/2}; W carries c'_{M/2}
+    const float v0 = zl.x + zl.y, vm = zl.x - zl.y;
+    const float2 wz = cmul(conj2(zh), W);
+    return make_float4(2.f * cA.x * v0, 2.f * cB.x * vm, 2.f * wz.x, -2.f * wz.y);
+  }
+  const float2 zc = conj2(zh);
+  const float2 P = cadd(zl, zc);
+  const float2 U = cmul(mul_ni(csub(zl, zc)), W);
+  const float2 wA = cmul(cadd(P, U), cA);
+  const float2 wB = cmul(conj2(csub(P, U)), cB);
+  return make_float4(wA.x, -wA.y, wB.x, -wB.y);
+}
+
+// DCT-III pre-pass of one slot: Y at the four bins -> G_k (gl), G_{M-k} (gh).
+__device__ __forceinline__ void hl_pre(float4 Y, float2 cA, float2 cB, float2 W, bool special, float2& gl,
+                                       float2& gh) {
+  if (special) {
+    const float f0 = 2.f * cA.x * Y.x, fm = 2.f * cB.x * Y.y;
+    gl = make_float2(f0 + fm, fm - f0);
+    const float2 F = cmul(make_float2(Y.z, -Y.w), conj2(W));
+    gh = make_float2(2.f * F.x, 2.f * F.y);
+    return;
+  }
+  const float2 Fk = cmul(make_float2(Y.x, -Y.y), conj2(cA));
+  const float2 Fmc = conj2(cmul(make_float2(Y.z, -Y.w), conj2(cB)));
+  const float2 A = cadd(Fk, Fmc);
+  const float2 D = csub(Fk, Fmc);
+  gl = cadd(conj2(A), mul_ni(cmul(conj2(D), W)));
+  gh = cadd(A, mul_ni(cmul(D, conj2(W))));
+}
+
+__device__ __forceinline__ float4 ld_row_f4(const float4* p) { return __ldg(p); }
+__device__ __forceinline__ float4 f4mul(float4 a, float4 b) { return make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w); }
+
+// Pass-0 inputs of one row: z[m] = (x[4m], x[4m+2]) kept, (x[4m+3], x[4m+1]) sent to the partner's slot 15-q.
+template <class G, bool SCALE>
+__device__ __forceinline__ void hl_load(float2 (&v)[16], const float* x, const float* sc, const FastMap<G>& fm) {
+  constexpr int S = FastMap<G>::S;
+  const float4* px = reinterpret_cast<const float4*>(x) + fm.jsp;
+  const float4* ps = reinterpret_cast<const float4*>(SCALE ? sc : x) + fm.jsp;
+  float2 snd[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    float4 f = ld_row_f4(px + q * S);
+    if constexpr (SCALE) f = f4mul(f, __ldg(ps + q * S));
+    v[q] = make_float2(f.x, f.z);
+    snd[q] = make_float2(f.w, f.y);
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[15 - q] = fm.xor_shfl(snd[q]);
+}
+
+// Last-pass outputs H[jsp + q*S] -> the row values at 4m..4m+3, m = jsp + q*S (q < 8).
+template <class G>
+__device__ __forceinline__ void hl_out(const float2 (&h)[16], float4 (&o)[8], const FastMap<G>& fm) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float2 r = fm.xor_shfl(h[15 - q]);
+    o[q] = make_float4(h[q].x, -r.y, -h[q].y, r.x);
+  }
+}
+
+// ------------------------------------------------------------------ forward
+// y = C3(d * C2(a * x) + bias) (layers.py:141-146), one row per group
+// iteration; H2C also stores h2 = C2(a x) as [row][slot][t] float4 (bins b0..b3).
+template <int LOGN, bool H2C>
+__global__ void ACDC_LB(GeoHL<LOGN>) acdc_fwd_hl_kernel(KParams p) {
+  using G = GeoHL<LOGN>;
+  constexpr int T = G::T;
+  pdl_launch_dependents();  // the backward may stage its prologue while this grid drains
+  extern __shared__ __align__(16) float smem_f[];
+  const auto c = group_ctx<G>();
+  const int t = c.t;
+  GroupSync<G> gs(c.grp);
+  Xbuf<G> xb{smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS, 0};
+  const float2 *tw, *cp, *wn;
+  stage_tables_hl<G>(p.tab, smem_f, tw, cp, wn);
+  const FastMap<G> fm(t, gs.mask);
+  for (int64_t r = c.gid; r < p.rows; r += c.gstride) {
+    if (t == 0 && r + c.gstride < p.rows) prefetch_row_l2(p.x + (r + c.gstride) * p.ldx, G::NR);
+    float2 v[16];
+    hl_load<G, true>(v, p.x + r * p.ldx, p.a, fm);
+    fft_passes<G, 0, true>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
+    {
+      float2 w[8], gl[8], gh[8];
+      fp_partner<G>(v, w, fm);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        float2 cA, cB, W;
+        hl_coefs<G>(cp, wn, fm, s, cA, cB, W);
+        const HlSlot<G> sl(fm, s);
+        float4 X = hl_post(v[s], w[s], cA, cB, W, sl.sp);
+        if constexpr (H2C) __stcs(reinterpret_cast<float4*>(p.h2c + r * G::NR) + s * T + t, X);
+        X.x = fmaf(X.x, ld_plain(p.d + sl.b[0]), ld_plain(p.bias + sl.b[0]));
+        X.y = fmaf(X.y, ld_plain(p.d + sl.b[1]), ld_plain(p.bias + sl.b[1]));
+        X.z = fmaf(X.z, ld_plain(p.d + sl.b[2]), ld_plain(p.bias + sl.b[2]));
+        X.w = fmaf(X.w, ld_plain(p.d + sl.b[3]), ld_plain(p.bias + sl.b[3]));
+        hl_pre(X, cA, cB, W, sl.sp, gl[s], gh[s]);
+      }
+      fp_scatter<G>(gl, gh, v, fm);
+    }
+    fft_passes<G, 0, true>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
+    float4 o[8];
+    hl_out<G>(v, o, fm);
+    float4* py = reinterpret_cast<float4*>(p.y + r * p.ldo) + fm.jsp;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) py[q * FastMap<G>::S] = o[q];
+  }
+}
+
+// ----------------------------------------------------------------- backward
+template <int LOGN>
+__host__ __device__ constexpr bool hl_tm_a() {  // grad_a also in TMEM (else: the CTA's partial row in global memory)
+  return (GeoHL<LOGN>::CTA / 128) * 96 <= 512;
+}
+template <int LOGN>
+__host__ __device__ constexpr int hl_ncol() {
+  return hl_tm_a<LOGN>() ? 96 : 64;
+}
+template <int LOGN>
+__host__ __device__ constexpr int hl_cols() {
+  constexpr int need = (GeoHL<LOGN>::CTA / 128) * hl_ncol<LOGN>();
+  return need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
+}
+
+__device__ __forceinline__ void tmem_ld16f(uint32_t a, float (&r)[16]) {
+  float2 v[8];
+  tmem_ld16(a, v);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r[2 * i] = v[i].x, r[2 * i + 1] = v[i].y;
+}
+__device__ __forceinline__ void tmem_st16f(uint32_t a, const float (&r)[16]) {
+  float2 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = make_float2(r[2 * i], r[2 * i + 1]);
+  tmem_st16(a, v);
+}
+
+// RECOMP: h2 = C2(a x) is recomputed instead of read from the cache.
+template <int LOGN, bool RECOMP>
+__global__ void ACDC_LB(GeoHL<LOGN>) acdc_bwd_hl_kernel(KParams p) {
+  using G = GeoHL<LOGN>;
+  constexpr int T = G::T;
+  constexpr int S = FastMap<G>::S;
+  constexpr bool TMA = hl_tm_a<LOGN>();
+  constexpr int NCOL = hl_ncol<LOGN>();
+  constexpr int COLS = hl_cols<LOGN>();
+  constexpr bool PRE = T <= 512;  // h2 of the row loaded across the dy transform (register budget)
+  pdl_launch_dependents();        // the reduction may launch early; it waits for this grid
+  extern __shared__ __align__(16) float smem_f[];
+  __shared__ uint32_t tm_slot;
+  const auto c = group_ctx<G>();
+  const int t = c.t;
+  const int warp = threadIdx.x >> 5;
+  GroupSync<G> gs(c.grp);
+  Xbuf<G> xb{smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS, 0};
+  const FastMap<G> fm(t, gs.mask);
+  if (warp == 0) tmem_alloc<COLS>(&tm_slot);
+  tmem_fence_before();
+  const float2 *tw, *cp, *wn;
+  stage_tables_hl<G>(p.tab, smem_f, tw, cp, wn);
+  if constexpr (!G::TW_SMEM) __syncthreads();
+  tmem_fence_after();
+  // columns: [16 sp, 16 sp + 16) = (b, d) bins of slots 2sp, 2sp+1; [64, 96) grad_a positions (TMA)
+  const uint32_t ta = tmem_addr(tm_slot, warp, (warp >> 2) * NCOL);
+  float* wsg = p.ws + c.gid * 3 * (int64_t)G::NR;  // this group's partial [3][N]: grad_a, grad_d, grad_bias
+  float4* gag = reinterpret_cast<float4*>(wsg) + fm.jsp;  // grad_a partial (global, !TMA)
+  {
+    float z[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) z[i] = 0.f;
+#pragma unroll
+    for (int k = 0; k < NCOL / 16; ++k) tmem_st16f(ta + 16 * k, z);
+    if constexpr (!TMA) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) gag[q * S] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  pdl_wait();  // x, dy (maybe the forward's y) and the h2 cache are read from here on
+  for (int64_t it = c.gid; it < p.rows; it += c.gstride) {
+    const int64_t r = p.rows - 1 - it;  // last-first: the forward's last rows are still in L2
+    if (t == 0 && it + c.gstride < p.rows) {
+      const int64_t nr = p.rows - 1 - (it + c.gstride);
+      prefetch_row_l2(p.dy + nr * p.ldy, G::NR);
+      prefetch_row_l2(p.x + nr * p.ldx, G::NR);
+    }
+    const float4* hc = reinterpret_cast<const float4*>(p.h2c + r * G::NR) + t;
+    float4 h2v[8];
+    float2 v[16];
+    if constexpr (RECOMP) {
+      hl_load<G, true>(v, p.x + r * p.ldx, p.a, fm);
+      fft_passes<G, 0, true>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
+      float2 w[8];
+      fp_partner<G>(v, w, fm);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        float2 cA, cB, W;
+        hl_coefs<G>(cp, wn, fm, s, cA, cB, W);
+        h2v[s] = hl_post(v[s], w[s], cA, cB, W, fm.special(s));
+      }
+    } else if constexpr (PRE) {
+#pragma unroll
+      for (int s = 0; s < 8; ++s) h2v[s] = __ldcs(hc + s * T);
+    }
+    hl_load<G, false>(v, p.dy + r * p.ldy, nullptr, fm);
+    fft_passes<G, 0, true>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
+    {
+      float2 w[8], gl[8], gh[8];
+      fp_partner<G>(v, w, fm);
+#pragma unroll
+      for (int sp = 0; sp < 4; ++sp) {
+        float acc[16];
+        tmem_ld16f(ta + 16 * sp, acc);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int s = 2 * sp + j;
+          float2 cA, cB, W;
+          hl_coefs<G>(cp, wn, fm, s, cA, cB, W);
+          const HlSlot<G> sl(fm, s);
+          const float4 g3 = hl_post(v[s], w[s], cA, cB, W, sl.sp);
+          const float4 h4 = (RECOMP || PRE) ? h2v[s] : __ldcs(hc + s * T);
+          float* ab = acc + 8 * j;
+          ab[0] += g3.x, ab[1] += g3.y, ab[2] += g3.z, ab[3] += g3.w;
+          ab[4] = fmaf(h4.x, g3.x, ab[4]), ab[5] = fmaf(h4.y, g3.y, ab[5]);
+          ab[6] = fmaf(h4.z, g3.z, ab[6]), ab[7] = fmaf(h4.w, g3.w, ab[7]);
+          const float4 y = make_float4(g3.x * ld_plain(p.d + sl.b[0]), g3.y * ld_plain(p.d + sl.b[1]),
+                                       g3.z * ld_plain(p.d + sl.b[2]), g3.w * ld_plain(p.d + sl.b[3]));
+          hl_pre(y, cA, cB, W, sl.sp, gl[s], gh[s]);
+        }
+        tmem_st16f(ta + 16 * sp, acc);
+      }
+      fp_scatter<G>(gl, gh, v, fm);
+    }
+    // x of this row: in flight across the g1 transform
+    float4 xv[8];
+    const float4* px = reinterpret_cast<const float4*>(p.x + r * p.ldx) + fm.jsp;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) xv[q] = ld_row_f4(px + q * S);
+    fft_passes<G, 0, true>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
+    float4 g1[8];
+    hl_out<G>(v, g1, fm);
+    const float4* pa = reinterpret_cast<const float4*>(p.a) + fm.jsp;
+    float4* po = reinterpret_cast<float4*>(p.y + r * p.ldo) + fm.jsp;
+    if constexpr (TMA) {
+#pragma unroll
+      for (int qp = 0; qp < 2; ++qp) {
+        float acc[16];
+        tmem_ld16f(ta + 64 + 16 * qp, acc);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int q = 4 * qp + j;
+          acc[4 * j] = fmaf(xv[q].x, g1[q].x, acc[4 * j]);
+          acc[4 * j + 1] = fmaf(xv[q].y, g1[q].y, acc[4 * j + 1]);
+          acc[4 * j + 2] = fmaf(xv[q].z, g1[q].z, acc[4 * j + 2]);
+          acc[4 * j + 3] = fmaf(xv[q].w, g1[q].w, acc[4 * j + 3]);
+        }
+        tmem_st16f(ta + 64 + 16 * qp, acc);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 gacc = gag[q * S];
+        gacc.x = fmaf(xv[q].x, g1[q].x, gacc.x);
+        gacc.y = fmaf(xv[q].y, g1[q].y, gacc.y);
+        gacc.z = fmaf(xv[q].z, g1[q].z, gacc.z);
+        gacc.w = fmaf(xv[q].w, g1[q].w, gacc.w);
+        gag[q * S] = gacc;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) po[q * S] = f4mul(__ldg(pa + q * S), g1[q]);
+  }
+  // this group's partials: grad_d / grad_bias at the slot bins, grad_a at 4m..4m+3
+#pragma unroll
+  for (int sp = 0; sp < 4; ++sp) {
+    float acc[16];
+    tmem_ld16f(ta + 16 * sp, acc);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const HlSlot<G> sl(fm, 2 * sp + j);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        wsg[2 * G::NR + sl.b[i]] = acc[8 * j + i];
+        wsg[G::NR + sl.b[i]] = acc[8 * j + 4 + i];
+      }
+    }
+  }
+  if constexpr (TMA) {
+#pragma unroll
+    for (int qp = 0; qp < 2; ++qp) {
+      float acc[16];
+      tmem_ld16f(ta + 64 + 16 * qp, acc);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        gag[(4 * qp + j) * S] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc<COLS>(tm_slot);
+}
+
+// ------------------------------------------------------------------ host
+#ifndef ACDC_HL_MIN_LOGN  // smallest size run on the half-length plan (the row-pair kernels below it)
+#define ACDC_HL_MIN_LOGN 13
+#endif
+
+template <class K>
+static void geom_hl(LaunchInfo& li) {
+  li.cta = K::CTA;
+  li.gpc = K::GPC;
+  li.smem = K::SMEM_BYTES;
+  li.unit_rows = 1;
+  li.hl = true;
+}
+
+template <int LOGN>
+static void hl_info(int kind, LaunchInfo* li) {
+  using G = GeoHL<LOGN>;
+  geom_hl<G>(*li);
+  switch (kind) {
+    case 0: li->fn = (const void*)acdc_fwd_hl_kernel<LOGN, false>; break;
+    case 4: li->fn = (const void*)acdc_fwd_hl_kernel<LOGN, true>; break;
+    case 1:
+    case 5:
+      li->fn = kind == 1 ? (const void*)acdc_bwd_hl_kernel<LOGN, true> : (const void*)acdc_bwd_hl_kernel<LOGN, false>;
+#ifndef ACDC_NO_PDL
+      li->pdl = true;
+#endif
+      li->max_per_sm = 512 / hl_cols<LOGN>();
+      break;
+    default: li->fn = nullptr;
+  }
+}
+
+// Launch description of the half-length kernel for (logn, kind), kinds as in
+// acdc_kernels.cu (0 fwd, 1 bwd recompute, 4 fwd + h2 cache, 5 bwd cached);
+// returns false when the size / kind is not on the half-length plan.  The
+// environment variable ACDC_HL=0 turns the plan off (A/B runs).
+bool hl_launch_info(int logn, int kind, LaunchInfo* li) {
+  static const bool on = [] {
+    const char* e = getenv("ACDC_HL");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || logn < ACDC_HL_MIN_LOGN || logn > 15) return false;
+  if (kind != 0 && kind != 1 && kind != 4 && kind != 5) return false;
+  switch (logn) {
+    case 13: hl_info<13>(kind, li); break;
+    case 14: hl_info<14>(kind, li); break;
+    case 15: hl_info<15>(kind, li); break;
+    default: return false;
+  }
+  return li->fn != nullptr;
+}
+
+bool hl_enabled(int logn) {
+  LaunchInfo li;
+  return hl_launch_info(logn, 0, &li);
+}
+
+}  // namespace acdc

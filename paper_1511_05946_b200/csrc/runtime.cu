@@ -74,12 +74,15 @@ static void host_plan(int logn, std::vector<int>& radix) {
   for (int p = 0; p < np; ++p) radix.push_back((rem && p == 1) ? (1 << rem) : 16);
 }
 
-int get_tables(int logn, Tables* out) {
+// hl: the half-length tables of a length-2^logn row (hl_kernels.cu): pass
+// twiddles of the 2^(logn-1)-point engine, c'_j for j <= N/2, then W_N^k for
+// k <= N/4.
+static int build_tables(int logn, bool hl, Tables* out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return set_cuda_error(e);
   std::lock_guard<std::mutex> lk(g_mu);
-  auto key = std::make_pair(dev, logn);
+  auto key = std::make_pair(dev, hl ? 100 + logn : logn);
   auto it = g_tables.find(key);
   if (it != g_tables.end()) {
     *out = it->second;
@@ -87,7 +90,7 @@ int get_tables(int logn, Tables* out) {
   }
   const int n = 1 << logn;
   std::vector<int> radix;
-  host_plan(logn, radix);
+  host_plan(hl ? logn - 1 : logn, radix);
   // per-pass [k][q] twiddle rows, stride Plan::tw_stride(R) (fft_engine.cuh)
   std::vector<float2> h;
   long ns = radix[0];
@@ -112,6 +115,8 @@ int get_tables(int logn, Tables* out) {
     const double th = pi * (double)k / (2.0 * n);
     h.push_back(make_float2((float)(s * std::cos(th)), (float)(-s * std::sin(th))));
   }
+  if (hl)
+    for (int k = 0; k <= n / 4; ++k) h.push_back(twiddle(k, n));
   Tables tb;
   if ((e = cudaMalloc(&tb.tab, sizeof(float2) * h.size())) != cudaSuccess) return set_cuda_error(e);
   if ((e = cudaMemcpy(tb.tab, h.data(), sizeof(float2) * h.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
@@ -120,6 +125,9 @@ int get_tables(int logn, Tables* out) {
   *out = tb;
   return ACDC_OK;
 }
+
+int get_tables(int logn, Tables* out) { return build_tables(logn, false, out); }
+int get_tables_hl(int logn, Tables* out) { return build_tables(logn, true, out); }
 
 int grid_for(const LaunchInfo& li, int64_t units, int64_t* grid) {
   int dev = 0;

@@ -17,6 +17,9 @@ struct Tables {
 
 // Build (once per device and size) and return the tables.
 int get_tables(int logn, Tables* out);
+// Half-length plan tables (hl_kernels.cu): [pass twiddles of Plan<logn-1> |
+// c'_j, j <= N/2 | W_N^k = e^{-2 pi i k/N}, k <= N/4].
+int get_tables_hl(int logn, Tables* out);
 
 // n must be a power of two in [1, 32768]; sets logn.
 int check_n(int32_t n, int* logn);
@@ -35,11 +38,18 @@ struct LaunchInfo {
   int max_per_sm = 0;  // cap on resident CTAs per SM (TMEM columns), 0 = occupancy only
   int red_per_cta = 0;  // gradient partials one CTA writes (0: one per group)
   bool pdl = false;     // programmatic dependent launch: may start while the previous kernel drains
+  int unit_rows = 2;    // rows one group handles per iteration (2: a row pair; 1: the half-length plan)
+  bool hl = false;      // half-length plan (hl_kernels.cu): its own tables
 };
 
 // Persistent grid: min(CTAs needed for `units` row groups, resident CTAs).
 // Sets the dynamic-smem attribute on first use.
 int grid_for(const LaunchInfo& li, int64_t units, int64_t* grid);
+
+// Half-length plan (hl_kernels.cu): launch description for (logn, kind) if
+// that size / kind runs on it; hl_enabled(logn): the size runs on it.
+bool hl_launch_info(int logn, int kind, LaunchInfo* li);
+bool hl_enabled(int logn);
 
 // Launch li.fn with one KParams-like argument struct.
 int launch(const LaunchInfo& li, int64_t grid, void* params, cudaStream_t st);

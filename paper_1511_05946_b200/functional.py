@@ -59,6 +59,8 @@ def _rows2d(x: torch.Tensor, n: int, name: str = "x") -> torch.Tensor:
         x = x.float()
     if x.stride(1) != 1 or (x.shape[0] > 1 and x.stride(0) < n):
         x = x.contiguous()
+    elif n >= 8192 and x.numel() and (x.data_ptr() % 16 or (x.shape[0] > 1 and x.stride(0) % 4)):
+        x = x.contiguous()  # the half-length large-N kernels move rows as 128-bit quads
     return x
 
 
@@ -90,7 +92,7 @@ def _check_out(out: torch.Tensor, like: torch.Tensor, name: str = "out", host_ok
 def _check_h2cache(h2cache: torch.Tensor, rows: int, n: int, dev) -> torch.Tensor:
     need = _lib.load().acdc_h2cache_bytes(rows, n)
     if need == 0:
-        raise ValueError(f"the h2 cache needs 256 <= n <= 16384, got {n}")
+        raise ValueError(f"the h2 cache needs 256 <= n <= 32768, got {n}")
     if (not isinstance(h2cache, torch.Tensor) or h2cache.device != dev or h2cache.dtype != torch.float32
             or not h2cache.is_contiguous() or h2cache.numel() * 4 < need):
         raise ValueError(f"h2cache must be a contiguous fp32 tensor on {dev} of at least {need} bytes "
@@ -105,15 +107,16 @@ def prepare(n: int, device=None) -> None:
 
 
 def h2cache_supported(n: int) -> bool:
-    """Sizes whose kernels can cache h2 = C2(a*x) between forward and backward."""
-    return 256 <= n <= 16384 and (n & (n - 1)) == 0
+    """Sizes whose kernels can cache h2 = C2(a*x) between forward and backward
+    (256 <= n <= 16384 on the row-pair kernels, up to 32768 on the half-length plan)."""
+    return 256 <= n <= 32768 and (n & (n - 1)) == 0 and _lib.load().acdc_h2cache_bytes(2, n) > 0
 
 
 def new_h2cache(rows: int, n: int, device) -> torch.Tensor:
     """Buffer for the h2 cache of ``rows`` rows (opaque, kernel-native layout)."""
     nbytes = _lib.load().acdc_h2cache_bytes(rows, n)
     if nbytes == 0:
-        raise ValueError(f"the h2 cache needs 256 <= n <= 16384, got {n}")
+        raise ValueError(f"the h2 cache needs 256 <= n <= 32768, got {n}")
     return torch.empty(nbytes // 4, dtype=torch.float32, device=device)
 
 
@@ -192,7 +195,7 @@ def acdc_backward(
 
 
 def acdc_backward_sgd(x, dy, params, velocities, lr, weight_decay, momentum, grads=None, accumulate=False, out=None,
-                      h2cache=None, prev_perm=None, prev_relu=False, ws=None) -> torch.Tensor:
+                      h2cache=None, prev_perm=None, prev_relu=False, ws=None, h2_rowpair=False) -> torch.Tensor:
     """Backward of one ACDC layer fused with its momentum-SGD step (reference
     AcdcLayer.backward + Sgd.step, layers.py:148-156, training.py:58-98).
 
@@ -201,7 +204,8 @@ def acdc_backward_sgd(x, dy, params, velocities, lr, weight_decay, momentum, gra
     the decay actually applied, per parameter).  ``grads`` (grad_a, grad_d,
     grad_bias) are added to the batch gradient when ``accumulate`` and zeroed.
     ``h2cache`` / ``prev_perm`` / ``prev_relu`` select the cached and fused-
-    cascade block backward.  Returns dx (computed with the pre-step a, d)."""
+    cascade block backward (``h2_rowpair``: the cache was written by the fused
+    cascade forward).  Returns dx (computed with the pre-step a, d)."""
     a = params[0]
     n = a.shape[0]
     x = _rows2d(x, n)
@@ -233,7 +237,8 @@ def acdc_backward_sgd(x, dy, params, velocities, lr, weight_decay, momentum, gra
         if ws is None or ws.numel() * 4 < wsb:
             ws = torch.empty((wsb + 3) // 4, dtype=torch.float32, device=dev)
         _lib.check(lib.acdc_bwd_sgd_f32(
-            _ptr(x), _ptr(dy), _ptr(dx), _ptr(h2cache), _ptr(prev_perm), 1 if prev_relu else 0, _ptr(g[0]),
+            _ptr(x), _ptr(dy), _ptr(dx), _ptr(h2cache), _ptr(prev_perm), (1 if prev_relu else 0) | (2 if h2_rowpair else 0),
+            _ptr(g[0]),
             _ptr(g[1]), _ptr(g[2]), 1 if accumulate else 0, ctypes.byref(st), _ptr(ws), wsb, x.shape[0], n,
             _ld(x, n), _ld(dy, n), _ld(dx, n), _stream(x)))
     return dx
@@ -418,7 +423,8 @@ def afdf(x, a, d):
 
 
 def cascade_supported(n: int) -> bool:
-    return h2cache_supported(n)
+    """Sizes of the fused cascade kernels (row-pair engine, h2 checkpoints)."""
+    return 256 <= n <= 16384 and (n & (n - 1)) == 0
 
 
 def cascade_forward(x: torch.Tensor, a: torch.Tensor, d: torch.Tensor, bias: torch.Tensor, perm: torch.Tensor | None,
@@ -499,7 +505,7 @@ def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor
             if sgd is not None:
                 prm, vel, lr3, wd3, mu = sgd[l]
                 acdc_backward_sgd(xl, g, prm, vel, lr3, wd3, mu, grads=(ga, gd, gb), accumulate=accumulate, out=out,
-                                  h2cache=h2[l], prev_perm=pp, prev_relu=bool(prev & 1), ws=ws)
+                                  h2cache=h2[l], prev_perm=pp, prev_relu=bool(prev & 1), ws=ws, h2_rowpair=True)
                 g = out
                 if on_block is not None:
                     on_block(l)

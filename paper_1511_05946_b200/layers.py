@@ -30,6 +30,7 @@ import numpy as np
 import torch
 
 from . import functional as F
+from .plans import DctPlan, FftPlan
 
 __all__ = [
     "Param",
@@ -133,34 +134,26 @@ class Layer:
         return y.detach().to("cpu", dtype=dt).numpy()
 
 
-@dataclass(frozen=True)
-class DctPlanInfo:
-    """What ``AcdcLayer.dct_plan`` exposes of the reference plan (transforms.py:86-95):
-    size, mode and backend; the tables themselves live in the CUDA library."""
-
-    n: int
-    mode: str
-    backend: str
-
-
 class AcdcLayer(Layer):
     """Diagonal, DCT, diagonal-with-bias, inverse DCT (layers.py:108-156).
 
-    ``backend`` accepts the reference values ("auto", "compiled", "python")
-    plus "b200"; all of them run the B200 kernels here.  ``dct_mode`` "naive"
-    is accepted for API parity and computes the same orthonormal transform.
+    ``dct_mode="fast"`` (power-of-two n) runs the fused sm_100a kernels.
+    ``dct_mode="naive"`` is the reference's cosine-matrix mode
+    (transforms.py:141, 152): any n >= 1, the transforms as dense fp32 GEMMs
+    with the explicit DCT matrix on the device (cuBLAS; O(N^2), not the hot
+    path).  ``backend`` takes the reference values ("auto", "compiled",
+    "python", env ``ACDC_KERNEL_BACKEND``) plus "b200"; all select the B200
+    kernels (``dct_plan.backend``).  ``dct_plan`` carries the reference
+    plan's tables (``plans.DctPlan``).
     """
 
     def __init__(self, n, dct_mode="fast", backend="auto", device=None, cache_h2=True):
-        if dct_mode not in ("naive", "fast"):
-            raise ValueError(f"unknown DCT mode {dct_mode!r}, expected one of ('naive', 'fast')")
-        if not _is_pow2(n):
-            raise ValueError(f"fast DCT requires a power-of-two size, got {n}")
+        self.dct_plan = DctPlan(n, mode=dct_mode, backend=backend)
         self.n_in = self.n_out = n
         self.dct_mode = dct_mode
         self.backend = backend
-        self.dct_plan = DctPlanInfo(n, dct_mode, "b200")
-        self.cache_h2 = bool(cache_h2) and F.h2cache_supported(n)
+        self.naive = dct_mode == "naive"
+        self.cache_h2 = bool(cache_h2) and not self.naive and F.h2cache_supported(n)
         self.device = _device(device)
         kw = dict(dtype=torch.float32, device=self.device)
         self.a = torch.ones(n, **kw)
@@ -175,7 +168,8 @@ class AcdcLayer(Layer):
             Param("bias_d", self.bias_d, self.grad_bias_d),
         ]
         self._cache = None
-        F.prepare(n, self.device)
+        if not self.naive:
+            F.prepare(n, self.device)
 
     @property
     def n(self):
@@ -189,6 +183,12 @@ class AcdcLayer(Layer):
 
     def forward(self, x):
         x, host = self._check_input(x)
+        if self.naive:  # h2 = (x a) C, y = (h2 d + b) C^T  (transforms.py:141, 152)
+            C = self.dct_plan.cos_device(self.device)
+            h2 = (x * self.a) @ C
+            y = torch.addcmul(self.bias_d, h2, self.d) @ C.t()
+            self._cache = (x, h2)
+            return self._out(y, host)
         hc = F.new_h2cache(x.shape[0], self.n_in, self.device) if (self.cache_h2 and x.shape[0]) else None
         y = F.acdc_forward(x, self.a, self.d, self.bias_d, h2cache=hc)
         self._cache = (x, hc)
@@ -199,6 +199,14 @@ class AcdcLayer(Layer):
         gy, host = self._check_input(grad_y)
         if gy.shape[0] != x.shape[0]:
             raise ValueError(f"grad_y has {gy.shape[0]} rows, forward input had {x.shape[0]}")
+        if self.naive:  # layers.py:148-156 with the dense transforms
+            C = self.dct_plan.cos_device(self.device)
+            g3 = gy @ C
+            self.grad_bias_d += g3.sum(0)
+            self.grad_d += (hc * g3).sum(0)
+            g1 = (g3 * self.d) @ C.t()
+            self.grad_a += (x * g1).sum(0)
+            return self._out(g1 * self.a, host)
         dx = F.acdc_backward(x, gy, self.a, self.d, self.grad_a, self.grad_d, self.grad_bias_d, accumulate=True,
                              h2cache=hc)
         return self._out(dx, host)
@@ -216,8 +224,7 @@ class AfdfLayer(Layer):
     complex_domain = True
 
     def __init__(self, n, backend="auto", fix_a=False, device=None):
-        if not _is_pow2(n):
-            raise ValueError(f"FFT size must be a power of two, got {n}")
+        self.fft_plan = FftPlan(n, backend=backend)  # transforms.py:69-83 (raises for non-powers of two)
         self.n_in = self.n_out = n
         self.backend = backend
         self.fix_a = fix_a
@@ -395,7 +402,7 @@ class Cascade:
             return None
         blocks, i = [], 0
         while i < len(layers):
-            if not isinstance(layers[i], AcdcLayer):
+            if not isinstance(layers[i], AcdcLayer) or layers[i].naive:
                 return None
             blk = [layers[i], None, None]
             i += 1

@@ -40,7 +40,9 @@ layer(1024, 12, True)     # TMEM backward (2 groups per CTA), odd row pairs per 
 layer(4096, 7, True)      # TMEM backward at the metric size, a ragged last pair
 layer(4096, 6, False)     # recompute backward
 layer(128, 2100, False)   # two-stage reduction (many row groups)
-layer(16384, 3, True)     # legacy cached backward, tables in global memory
+layer(16384, 3, True)     # half-length plan (N/2-point FFT per row), TMEM accumulators
+layer(32768, 2, True)     # half-length plan, tables in global memory, grad_a partial in global memory
+layer(8192, 5, False)     # half-length recompute backward
 # SGD-fused reduction, then a backward of the same layer (PDL ordering)
 n, rows = 1024, 10
 x, dy = rn(rows, n), rn(rows, n)

@@ -1,6 +1,6 @@
 """Summarise an ncu --set full report (and optional launch-list CSV) into profiles/.
 
-usage: python scripts/summarize_ncu.py <prof.ncu-rep> <out_dir> [launches.csv]
+usage: python scripts/summarize_ncu.py <prof.ncu-rep> <out_dir> [launches.csv] [--name NAME] [--traffic PATH]
 
 Writes <out_dir>/ncu_summary.md (per-kernel key metrics, instruction mix) and
 updates profiles/traffic.json (dram read+write bytes per launch, per kernel)
@@ -51,8 +51,15 @@ def short(name):
 
 
 def main():
-    rep, out_dir = sys.argv[1], sys.argv[2]
-    launches = sys.argv[3] if len(sys.argv) > 3 else None
+    argv = list(sys.argv[1:])
+    opts = {}
+    for key in ("--name", "--traffic"):
+        if key in argv:
+            i = argv.index(key)
+            opts[key] = argv[i + 1]
+            del argv[i:i + 2]
+    rep, out_dir = argv[0], argv[1]
+    launches = argv[2] if len(argv) > 2 else None
     os.makedirs(out_dir, exist_ok=True)
     rows = ncu_csv(["-i", rep, "--page", "raw"])
     hdr, units = rows[0], rows[1]
@@ -130,9 +137,10 @@ def main():
             lines.append("")
         except StopIteration:
             pass
-    with open(os.path.join(out_dir, "ncu_summary.md"), "w") as f:
+    with open(os.path.join(out_dir, opts.get("--name", "ncu_summary") + ".md"), "w") as f:
         f.write("\n".join(lines) + "\n")
-    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "traffic.json")
+    tpath = opts.get("--traffic") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles",
+                                                  "traffic.json")
     old = json.load(open(tpath)) if os.path.exists(tpath) else {}
     old.update(traffic)
     with open(tpath, "w") as f:

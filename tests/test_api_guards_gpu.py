@@ -132,3 +132,39 @@ def test_train_accepts_bare_layer():
     layer = AcdcLayer(32)
     losses = train(layer, ds, SgdConfig(learning_rate=0.01), epochs=2, batch_size=64)
     assert len(losses) == 2 and all(np.isfinite(losses))
+
+
+@pytest.mark.parametrize("n", [100, 256])
+def test_naive_mode_layer(n):
+    """dct_mode="naive" (transforms.py:141, 152): any n, dense transforms;
+    matches the fp64 oracle (and the fast layer where n is a power of two)."""
+    from paper_1511_05946_b200 import AcdcLayer
+
+    rng = np.random.default_rng(n)
+    rows = 9
+    L = AcdcLayer(n, dct_mode="naive")
+    assert L.dct_plan.backend == "naive" and L.dct_plan.cos_matrix.shape == (n, n)
+    a, d, b = 1 + 0.3 * rng.standard_normal(n), 1 + 0.3 * rng.standard_normal(n), 0.2 * rng.standard_normal(n)
+    for t, v in ((L.a, a), (L.d, d), (L.bias_d, b)):
+        t.copy_(torch.as_tensor(v, dtype=torch.float32))
+    x, dy = rng.standard_normal((rows, n)).astype(np.float32), rng.standard_normal((rows, n)).astype(np.float32)
+    y = L.forward(x)  # host in -> fp64 numpy out
+    dx = L.backward(dy)
+    A, D, B = (t.double().cpu().numpy() for t in (L.a, L.d, L.bias_d))
+    C = O.dct_matrix(n)
+    h2 = (x * A) @ C
+    yr = (h2 * D + B) @ C.T
+    g3 = dy.astype(np.float64) @ C
+    g1 = (g3 * D) @ C.T
+    assert np.abs(y - yr).max() <= 4 * O.fp32_tolerance(n, yr)
+    assert np.abs(dx - g1 * A).max() <= 4 * O.fp32_tolerance(n, g1 * A)
+    for mine, ref in ((L.grad_bias_d, g3.sum(0)), (L.grad_d, (h2 * g3).sum(0)), (L.grad_a, (x * g1).sum(0))):
+        assert np.abs(mine.double().cpu().numpy() - ref).max() <= 4 * O.grad_tolerance(n, rows, ref)
+    if n == 256:
+        F_ = AcdcLayer(n)
+        for t, v in ((F_.a, a), (F_.d, d), (F_.bias_d, b)):
+            t.copy_(torch.as_tensor(v, dtype=torch.float32))
+        assert np.abs(F_.forward(x) - y).max() <= 4 * O.fp32_tolerance(n, yr)
+    from paper_1511_05946_b200 import AfdfLayer
+
+    assert AfdfLayer(64).fft_plan.twiddle.shape == (32,)

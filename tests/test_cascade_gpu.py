@@ -75,7 +75,8 @@ def oracle_with_masks(x, dy, specs, casc, rows):
 
 @pytest.mark.parametrize("n,depth,rows,relu,perm", [(256, 3, 5, True, True), (1024, 12, 64, True, True),
                                                     (1024, 4, 33, False, True), (4096, 3, 16, True, False),
-                                                    (512, 1, 7, False, False)])
+                                                    (512, 1, 7, False, False), (8192, 2, 5, True, True),
+                                                    (16384, 2, 3, True, False)])
 def test_fused_cascade_vs_oracle(n, depth, rows, relu, perm):
     rng = np.random.default_rng(n * 7 + depth)
     casc, layers, specs = build(n, depth, rng, relu, perm)

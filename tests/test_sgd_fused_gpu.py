@@ -107,12 +107,14 @@ def test_fused_step_equals_unfused_path():
     assert opts[1].step_count == 3
 
 
-@pytest.mark.parametrize("fused_stack", [True, False])
-def test_cascade_backward_step(fused_stack):
+@pytest.mark.parametrize("fused_stack,n", [(True, 256), (False, 256), (True, 8192), (False, 16384)])
+def test_cascade_backward_step(fused_stack, n):
+    """n >= 8192: the fused stack's block backward reads the cascade's row-pair
+    h2 layout, the per-layer path the half-length layer kernels."""
     from paper_1511_05946_b200 import AcdcLayer, Cascade, PermutationLayer, ReluLayer
     from paper_1511_05946_b200 import training as T
 
-    n, rows, depth = 256, 48, 3
+    rows, depth = 48, 3
     rng = np.random.default_rng(11)
     perms = [rng.permutation(n) for _ in range(depth)]
     init = [(f32(rng, n, mean=1.0, std=0.2), f32(rng, n, mean=1.0, std=0.2), f32(rng, n, std=0.1))
