@@ -180,6 +180,20 @@ int afdf_bwd_c64(const float* x, const float* dy, float* dx, const float* a, con
 int acdc_fft_c64(const float* z, float* out, int64_t rows, int32_t n, int inverse, int64_t ldz, int64_t ldo,
                  acdc_stream_t stream);
 
+/* ---- ReLU and Permutation layers outside the fused cascade (layers.py:218-265) ----
+ * acdc_relu_fwd_f32: y = x > 0 ? x : 0 (strict mask, layers.py:227).
+ * acdc_relu_bwd_f32: dx = y > 0 ? dy : 0, with y the forward's OUTPUT
+ *   (y > 0 exactly where x > 0, layers.py:231-233).
+ * acdc_gather_cols: y[r, j] = x[r, idx[j]] for elem_bytes 4 (fp32) or 8
+ *   (complex64): the permutation forward with idx = perm and its backward
+ *   with idx = argsort(perm) (layers.py:254-265).  Not in place. */
+int acdc_relu_fwd_f32(const float* x, float* y, int64_t rows, int32_t n, int64_t ldx, int64_t ldy,
+                      acdc_stream_t stream);
+int acdc_relu_bwd_f32(const float* y, const float* dy, float* dx, int64_t rows, int32_t n, int64_t ldy, int64_t lddy,
+                      int64_t lddx, acdc_stream_t stream);
+int acdc_gather_cols(const void* x, void* y, const int32_t* idx, int64_t rows, int32_t n, int32_t elem_bytes,
+                     int64_t ldx, int64_t ldy, acdc_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

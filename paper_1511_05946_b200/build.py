@@ -66,9 +66,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = _nvcc()
     objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in sources()]
     flags = [f for f in NVCC_FLAGS if f != "-shared"]
-    jobs = [[nvcc, *flags, "-c", s, "-o", o] for s, o in zip(sources(), objs)]
-    with ThreadPoolExecutor(len(jobs)) as ex:
-        list(ex.map(lambda c: _run(c, verbose), jobs))
+    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
+        glob.glob(os.path.join(ROOT, "include", "*.h"))
+    newest_header = max((os.path.getmtime(h) for h in headers), default=0.0)
+
+    def fresh(src, obj):  # object newer than its source and every header (headers are shared)
+        return (not force and os.path.exists(obj) and os.path.getmtime(obj) >= os.path.getmtime(src)
+                and os.path.getmtime(obj) >= newest_header)
+
+    jobs = [[nvcc, *flags, "-c", s, "-o", o] for s, o in zip(sources(), objs) if not fresh(s, o)]
+    if jobs:
+        with ThreadPoolExecutor(len(jobs)) as ex:
+            list(ex.map(lambda c: _run(c, verbose), jobs))
     tmp = LIB + ".tmp"
     _run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", tmp], verbose)
     os.replace(tmp, LIB)

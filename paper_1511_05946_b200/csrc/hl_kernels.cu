@@ -43,9 +43,9 @@
 
 namespace acdc {
 
-template <int LOGN>
-struct GeoHL : Geo<LOGN - 1> {
-  using B = Geo<LOGN - 1>;
+template <int LOGN, int GPCX = 0>
+struct GeoHL : Geo<LOGN - 1, 0, GPCX> {
+  using B = Geo<LOGN - 1, 0, GPCX>;
   static constexpr int NR = 1 << LOGN;  // row length
   static constexpr int M = B::N;        // complex FFT length
   static constexpr int CPH = M + 1;     // c'_j, j <= N/2
@@ -177,21 +177,53 @@ __device__ __forceinline__ void hl_out(const float2 (&h)[16], float4 (&o)[8], co
 }
 
 // ------------------------------------------------------------------ forward
+#ifndef ACDC_HL_FWD_CTA  // forward CTA size where a group is 256 threads (N = 8192): 3 groups, 85 registers
+#define ACDC_HL_FWD_CTA 768
+#endif
+template <int LOGN>
+constexpr int hl_fwd_gpc() {
+  return (Geo<LOGN - 1>::T == 256 && ACDC_HL_FWD_CTA == 768) ? 3 : 0;
+}
+template <int LOGN>
+using GeoHLF = GeoHL<LOGN, hl_fwd_gpc<LOGN>()>;
+// d / bias of every thread's 8 spectral slots (32 bins) staged once per launch
+// in tensor memory, [slot] x (d0..d3, b0..b3), one tcgen05.ld per slot.
+template <int LOGN>
+__host__ __device__ constexpr int hl_fwd_cols() {
+  constexpr int need = (GeoHLF<LOGN>::CTA / 128) * 64;
+  return need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
+}
 // y = C3(d * C2(a * x) + bias) (layers.py:141-146), one row per group
 // iteration; H2C also stores h2 = C2(a x) as [row][slot][t] float4 (bins b0..b3).
 template <int LOGN, bool H2C>
-__global__ void ACDC_LB(GeoHL<LOGN>) acdc_fwd_hl_kernel(KParams p) {
-  using G = GeoHL<LOGN>;
+__global__ void ACDC_LB(GeoHLF<LOGN>) acdc_fwd_hl_kernel(KParams p) {
+  using G = GeoHLF<LOGN>;
   constexpr int T = G::T;
+  constexpr int COLS = hl_fwd_cols<LOGN>();
   pdl_launch_dependents();  // the backward may stage its prologue while this grid drains
   extern __shared__ __align__(16) float smem_f[];
+  __shared__ uint32_t tm_slot;
   const auto c = group_ctx<G>();
   const int t = c.t;
+  const int warp = threadIdx.x >> 5;
   GroupSync<G> gs(c.grp);
   Xbuf<G> xb{smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS, 0};
+  const FastMap<G> fm(t, gs.mask);
+  if (warp == 0) tmem_alloc<COLS>(&tm_slot);
+  tmem_fence_before();
   const float2 *tw, *cp, *wn;
   stage_tables_hl<G>(p.tab, smem_f, tw, cp, wn);
-  const FastMap<G> fm(t, gs.mask);
+  if constexpr (!G::TW_SMEM) __syncthreads();
+  tmem_fence_after();
+  const uint32_t ta = tmem_addr(tm_slot, warp, (warp >> 2) * 64);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const HlSlot<G> sl(fm, s);
+    float db[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) db[i] = __ldg(p.d + sl.b[i]), db[4 + i] = __ldg(p.bias + sl.b[i]);
+    tmem_st8(ta + 8 * s, db);
+  }
   for (int64_t r = c.gid; r < p.rows; r += c.gstride) {
     if (t == 0 && r + c.gstride < p.rows) prefetch_row_l2(p.x + (r + c.gstride) * p.ldx, G::NR);
     float2 v[16];
@@ -207,10 +239,12 @@ __global__ void ACDC_LB(GeoHL<LOGN>) acdc_fwd_hl_kernel(KParams p) {
         const HlSlot<G> sl(fm, s);
         float4 X = hl_post(v[s], w[s], cA, cB, W, sl.sp);
         if constexpr (H2C) __stcs(reinterpret_cast<float4*>(p.h2c + r * G::NR) + s * T + t, X);
-        X.x = fmaf(X.x, ld_plain(p.d + sl.b[0]), ld_plain(p.bias + sl.b[0]));
-        X.y = fmaf(X.y, ld_plain(p.d + sl.b[1]), ld_plain(p.bias + sl.b[1]));
-        X.z = fmaf(X.z, ld_plain(p.d + sl.b[2]), ld_plain(p.bias + sl.b[2]));
-        X.w = fmaf(X.w, ld_plain(p.d + sl.b[3]), ld_plain(p.bias + sl.b[3]));
+        float db[8];
+        tmem_ld8(ta + 8 * s, db);
+        X.x = fmaf(X.x, db[0], db[4]);
+        X.y = fmaf(X.y, db[1], db[5]);
+        X.z = fmaf(X.z, db[2], db[6]);
+        X.w = fmaf(X.w, db[3], db[7]);
         hl_pre(X, cA, cB, W, sl.sp, gl[s], gh[s]);
       }
       fp_scatter<G>(gl, gh, v, fm);
@@ -222,6 +256,10 @@ __global__ void ACDC_LB(GeoHL<LOGN>) acdc_fwd_hl_kernel(KParams p) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) py[q * FastMap<G>::S] = o[q];
   }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc<COLS>(tm_slot);
 }
 
 // ----------------------------------------------------------------- backward
@@ -230,8 +268,12 @@ __host__ __device__ constexpr bool hl_tm_a() {  // grad_a also in TMEM (else: th
   return (GeoHL<LOGN>::CTA / 128) * 96 <= 512;
 }
 template <int LOGN>
+__host__ __device__ constexpr bool hl_tm_d() {  // d of the 32 slot bins also in TMEM (cols 96..127)
+  return (GeoHL<LOGN>::CTA / 128) * 128 <= 512;
+}
+template <int LOGN>
 __host__ __device__ constexpr int hl_ncol() {
-  return hl_tm_a<LOGN>() ? 96 : 64;
+  return hl_tm_d<LOGN>() ? 128 : (hl_tm_a<LOGN>() ? 96 : 64);
 }
 template <int LOGN>
 __host__ __device__ constexpr int hl_cols() {
@@ -291,6 +333,19 @@ __global__ void ACDC_LB(GeoHL<LOGN>) acdc_bwd_hl_kernel(KParams p) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) gag[q * S] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    if constexpr (hl_tm_d<LOGN>()) {
+#pragma unroll
+      for (int sp = 0; sp < 4; ++sp) {
+        float dd[8];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const HlSlot<G> sl(fm, 2 * sp + j);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dd[4 * j + i] = __ldg(p.d + sl.b[i]);
+        }
+        tmem_st8(ta + 96 + 8 * sp, dd);
+      }
+    }
   }
   pdl_wait();  // x, dy (maybe the forward's y) and the h2 cache are read from here on
   for (int64_t it = c.gid; it < p.rows; it += c.gstride) {
@@ -325,8 +380,9 @@ __global__ void ACDC_LB(GeoHL<LOGN>) acdc_bwd_hl_kernel(KParams p) {
       fp_partner<G>(v, w, fm);
 #pragma unroll
       for (int sp = 0; sp < 4; ++sp) {
-        float acc[16];
+        float acc[16], dd[8];
         tmem_ld16f(ta + 16 * sp, acc);
+        if constexpr (hl_tm_d<LOGN>()) tmem_ld8(ta + 96 + 8 * sp, dd);
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int s = 2 * sp + j;
@@ -339,8 +395,13 @@ __global__ void ACDC_LB(GeoHL<LOGN>) acdc_bwd_hl_kernel(KParams p) {
           ab[0] += g3.x, ab[1] += g3.y, ab[2] += g3.z, ab[3] += g3.w;
           ab[4] = fmaf(h4.x, g3.x, ab[4]), ab[5] = fmaf(h4.y, g3.y, ab[5]);
           ab[6] = fmaf(h4.z, g3.z, ab[6]), ab[7] = fmaf(h4.w, g3.w, ab[7]);
-          const float4 y = make_float4(g3.x * ld_plain(p.d + sl.b[0]), g3.y * ld_plain(p.d + sl.b[1]),
-                                       g3.z * ld_plain(p.d + sl.b[2]), g3.w * ld_plain(p.d + sl.b[3]));
+          float4 y;
+          if constexpr (hl_tm_d<LOGN>()) {
+            y = make_float4(g3.x * dd[4 * j], g3.y * dd[4 * j + 1], g3.z * dd[4 * j + 2], g3.w * dd[4 * j + 3]);
+          } else {
+            y = make_float4(g3.x * ld_plain(p.d + sl.b[0]), g3.y * ld_plain(p.d + sl.b[1]),
+                            g3.z * ld_plain(p.d + sl.b[2]), g3.w * ld_plain(p.d + sl.b[3]));
+          }
           hl_pre(y, cA, cB, W, sl.sp, gl[s], gh[s]);
         }
         tmem_st16f(ta + 16 * sp, acc);
@@ -433,11 +494,15 @@ static void geom_hl(LaunchInfo& li) {
 
 template <int LOGN>
 static void hl_info(int kind, LaunchInfo* li) {
+  if (kind == 0 || kind == 4) {
+    geom_hl<GeoHLF<LOGN>>(*li);
+    li->fn = kind == 0 ? (const void*)acdc_fwd_hl_kernel<LOGN, false> : (const void*)acdc_fwd_hl_kernel<LOGN, true>;
+    li->max_per_sm = 512 / hl_fwd_cols<LOGN>();
+    return;
+  }
   using G = GeoHL<LOGN>;
   geom_hl<G>(*li);
   switch (kind) {
-    case 0: li->fn = (const void*)acdc_fwd_hl_kernel<LOGN, false>; break;
-    case 4: li->fn = (const void*)acdc_fwd_hl_kernel<LOGN, true>; break;
     case 1:
     case 5:
       li->fn = kind == 1 ? (const void*)acdc_bwd_hl_kernel<LOGN, true> : (const void*)acdc_bwd_hl_kernel<LOGN, false>;

@@ -39,6 +39,9 @@ __all__ = [
     "cascade_forward",
     "cascade_backward",
     "HostPipeline",
+    "relu_forward",
+    "relu_backward",
+    "gather_cols",
 ]
 
 
@@ -659,3 +662,45 @@ class HostPipeline:
             cur.wait_stream(s)
         if timeline:  # (upload, compute, download) completion events per chunk
             return list(zip(up, done, down))
+
+
+# ------------------------------------------------- ReLU / permutation layers
+
+
+def relu_forward(x: torch.Tensor) -> torch.Tensor:
+    """y = x > 0 ? x : 0 (layers.py:225-229), native kernel."""
+    x = _rows2d(x, x.shape[1])
+    y = torch.empty_like(x, memory_format=torch.contiguous_format)
+    with torch.cuda.device(x.device):
+        _lib.check(_lib.load().acdc_relu_fwd_f32(_ptr(x), _ptr(y), x.shape[0], x.shape[1], _ld(x, x.shape[1]),
+                                                 x.shape[1], _stream(x)))
+    return y
+
+
+def relu_backward(y: torch.Tensor, dy: torch.Tensor) -> torch.Tensor:
+    """dx = y > 0 ? dy : 0 with y the forward output (layers.py:231-233)."""
+    n = y.shape[1]
+    y, dy = _rows2d(y, n, "y"), _rows2d(dy, n, "grad_y")
+    if dy.shape != y.shape:
+        raise ValueError(f"grad_y has shape {tuple(dy.shape)}, the forward output {tuple(y.shape)}")
+    dx = torch.empty_like(dy, memory_format=torch.contiguous_format)
+    with torch.cuda.device(y.device):
+        _lib.check(_lib.load().acdc_relu_bwd_f32(_ptr(y), _ptr(dy), _ptr(dx), y.shape[0], n, _ld(y, n), _ld(dy, n),
+                                                 n, _stream(y)))
+    return dx
+
+
+def gather_cols(x: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
+    """y[:, j] = x[:, idx[j]] for fp32 or complex64 rows (idx int32 on the device)."""
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dim() != 2:
+        raise ValueError("expected a 2-D CUDA tensor")
+    if x.dtype not in (torch.float32, torch.complex64):
+        x = x.to(torch.complex64 if x.is_complex() else torch.float32)
+    if x.stride(1) != 1 or (x.shape[0] > 1 and x.stride(0) < x.shape[1]):
+        x = x.contiguous()
+    n = x.shape[1]
+    y = torch.empty_like(x, memory_format=torch.contiguous_format)
+    with torch.cuda.device(x.device):
+        _lib.check(_lib.load().acdc_gather_cols(_ptr(x), _ptr(y), _ptr(idx), x.shape[0], n, x.element_size(),
+                                                _ld(x, n), n, _stream(x)))
+    return y

@@ -280,13 +280,14 @@ class ReluLayer(Layer):
 
     def forward(self, x):
         x, host = self._check_input(x)
-        self._cache = x > 0
-        return self._out(torch.clamp_min(x, 0.0), host)
+        y = F.relu_forward(x)
+        self._cache = y  # y > 0 exactly where x > 0: the strict mask
+        return self._out(y, host)
 
     def backward(self, grad_y, retain_cache=False):
-        mask = self._take_cache(retain_cache)
+        y = self._take_cache(retain_cache)
         gy, host = self._check_input(grad_y)
-        return self._out(gy * mask, host)
+        return self._out(F.relu_backward(y, gy), host)
 
 
 class PermutationLayer(Layer):
@@ -304,8 +305,8 @@ class PermutationLayer(Layer):
             raise ValueError("perm is not a bijection on 0..n-1")
         self.perm = perm
         self.inverse_perm = np.argsort(perm)
-        self._perm_t = torch.as_tensor(perm, device=self.device)
-        self._inv_t = torch.as_tensor(self.inverse_perm, device=self.device)
+        self._perm_t = torch.as_tensor(perm, dtype=torch.int32, device=self.device)
+        self._inv_t = torch.as_tensor(self.inverse_perm, dtype=torch.int32, device=self.device)
         self._cache = None
 
     @staticmethod
@@ -320,12 +321,12 @@ class PermutationLayer(Layer):
             raise ValueError(f"PermutationLayer expects (batch, {self.n_in}) input")
         x, host = self._check_input(x, self._dtype(x))
         self._cache = True
-        return self._out(x.index_select(1, self._perm_t), host)
+        return self._out(F.gather_cols(x, self._perm_t), host)
 
     def backward(self, grad_y, retain_cache=False):
         self._take_cache(retain_cache)
         gy, host = self._check_input(grad_y, self._dtype(grad_y))
-        return self._out(gy.index_select(1, self._inv_t), host)
+        return self._out(F.gather_cols(gy, self._inv_t), host)
 
 
 class DenseLayer(Layer):

@@ -168,3 +168,34 @@ def test_naive_mode_layer(n):
     from paper_1511_05946_b200 import AfdfLayer
 
     assert AfdfLayer(64).fft_plan.twiddle.shape == (32,)
+
+
+@pytest.mark.parametrize("n,rows,cplx", [(7, 5, False), (1000, 33, True), (32768, 3, True), (16384, 4, False)])
+def test_relu_perm_native_layers(n, rows, cplx):
+    """ReluLayer / PermutationLayer outside the fused cascade run the native
+    kernels (layers.py:218-265): strict mask, gather by perm, scatter by
+    argsort(perm); complex rows permute as 8-byte elements."""
+    from paper_1511_05946_b200 import PermutationLayer, ReluLayer
+
+    rng = np.random.default_rng(n)
+    p = rng.permutation(n)
+    x = rng.standard_normal((rows, n)).astype(np.float32)
+    x[0, : min(n, 3)] = 0.0  # exact zeros: masked (strict x > 0)
+    if cplx:
+        xc = (x + 1j * rng.standard_normal((rows, n))).astype(np.complex64)
+        P = PermutationLayer(n, perm=p)
+        y = P.forward(torch.as_tensor(xc, device=DEV))
+        assert torch.equal(y.cpu(), torch.as_tensor(xc)[:, p])
+        g = P.backward(y)
+        assert torch.equal(g.cpu(), torch.as_tensor(xc))
+        return
+    R = ReluLayer(n)
+    y = R.forward(torch.as_tensor(x, device=DEV))
+    assert torch.equal(y.cpu(), torch.as_tensor(np.where(x > 0, x, 0.0).astype(np.float32)))
+    dy = rng.standard_normal((rows, n)).astype(np.float32)
+    dx = R.backward(torch.as_tensor(dy, device=DEV))
+    assert torch.equal(dx.cpu(), torch.as_tensor(np.where(x > 0, dy, 0.0).astype(np.float32)))
+    P = PermutationLayer(n, perm=p)
+    yp = P.forward(torch.as_tensor(x, device=DEV))
+    assert torch.equal(yp.cpu(), torch.as_tensor(x[:, p]))
+    assert torch.equal(P.backward(yp).cpu(), torch.as_tensor(x))
