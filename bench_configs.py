@@ -117,6 +117,24 @@ def c1(args, dev):
             "speedup_vs_cpu": rps / rps_cpu}
 
 
+def graphed(step):
+    """The step captured once in a CUDA graph (the kernels' programmatic
+    dependent launches are kept); replaying it removes the Python / ctypes
+    launch overhead, which exceeds the GPU time at small N."""
+    step()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        step()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=s):
+            step()
+    torch.cuda.synchronize()
+    return graph.replay
+
+
 def sweep(args, dev):
     out = []
     hbm = peak_hbm()
@@ -124,9 +142,11 @@ def sweep(args, dev):
         n = 1 << lg
         B = 16384
         step, mode = layer_step(n, B, dev)
-        ms = timeit(step, args.steps)
+        ms_eager = timeit(step, args.steps)
+        ms = timeit(graphed(step), args.steps)
         rps = B / (ms / 1e3)
-        row = {"config": "sweep single ACDC layer fwd+bwd batch 16384", "n": n, "mode": mode, "ms_per_step": ms,
+        row = {"config": "sweep single ACDC layer fwd+bwd batch 16384 (CUDA-graph replay)", "n": n, "mode": mode,
+               "ms_per_step": ms, "ms_per_step_eager": ms_eager,
                "rows_per_s": rps, "hbm_roofline_frac_20N": rps * 20 * n / (hbm * 1e9)}
         if n <= 8192:
             for tf32 in (False, True):

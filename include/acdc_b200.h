@@ -180,6 +180,20 @@ int afdf_bwd_c64(const float* x, const float* dy, float* dx, const float* a, con
 int acdc_fft_c64(const float* z, float* out, int64_t rows, int32_t n, int inverse, int64_t ldz, int64_t ldo,
                  acdc_stream_t stream);
 
+/* Fused-cascade block backward with the permutation moved from the next
+ * block's epilogue (a scattered store) to this block's dy load (a gather):
+ * dy[:, i] = dy_in[:, dy_gather[i]] with dy_gather = argsort(perm) of the
+ * permutation that follows this block; prev_relu masks this block's dx by
+ * x > 0 (the previous block's ReLU), which is then written unpermuted.  Only
+ * where the TMEM backward runs (cascade_gather_supported(n) != 0, 512 <= n <=
+ * 8192); ACDC_E_SIZE otherwise (use cascade_bwd_block_f32). */
+int cascade_gather_supported(int32_t n);
+int cascade_bwd_block_gather_f32(const float* x, const float* dy, float* dx, const float* a, const float* d,
+                                 const float* h2cache, const int32_t* dy_gather, int prev_relu, float* grad_a,
+                                 float* grad_d, float* grad_bias, int accumulate, void* ws, size_t ws_bytes,
+                                 int64_t rows, int32_t n, int64_t ldx, int64_t ldy, int64_t lddx,
+                                 acdc_stream_t stream);
+
 /* ---- ReLU and Permutation layers outside the fused cascade (layers.py:218-265) ----
  * acdc_relu_fwd_f32: y = x > 0 ? x : 0 (strict mask, layers.py:227).
  * acdc_relu_bwd_f32: dx = y > 0 ? dy : 0, with y the forward's OUTPUT

@@ -776,14 +776,34 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
       mbar_wait(bar, parity);
       parity ^= 1u;
       float2 pa[8], pb[8];
-      const float2* sa = reinterpret_cast<const float2*>(stg) + fm.jsp;
+      if (p.dy_gather) {  // fused cascade: dy[:, i] = dx_next[:, inv_perm[i]], gathered from the staged rows
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        pa[q] = sa[q * S];
-        pb[q] = hasb ? sa[G::N / 2 + q * S] : make_float2(0.f, 0.f);
+        for (int q = 0; q < 8; ++q) {
+          const int2 iv = __ldg(reinterpret_cast<const int2*>(p.dy_gather) + fm.jsp + q * S);
+          pa[q] = make_float2(stg[iv.x], stg[iv.y]);
+          pb[q] = hasb ? make_float2(stg[G::N + iv.x], stg[G::N + iv.y]) : make_float2(0.f, 0.f);
+        }
+      } else {
+        const float2* sa = reinterpret_cast<const float2*>(stg) + fm.jsp;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          pa[q] = sa[q * S];
+          pb[q] = hasb ? sa[G::N / 2 + q * S] : make_float2(0.f, 0.f);
+        }
       }
       fp_from_pairs<G>(v, pa, pb, fm);
       gs.sync();  // buffer A is read by every thread before exchange 1 writes it
+    } else if (p.dy_gather) {
+      float2 pa[8], pb[8];
+      const float* ya = p.dy + ra * p.ldy;
+      const float* yb = p.dy + rb * p.ldy;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int2 iv = __ldg(reinterpret_cast<const int2*>(p.dy_gather) + fm.jsp + q * S);
+        pa[q] = make_float2(__ldg(ya + iv.x), __ldg(ya + iv.y));
+        pb[q] = hasb ? make_float2(__ldg(yb + iv.x), __ldg(yb + iv.y)) : make_float2(0.f, 0.f);
+      }
+      fp_from_pairs<G>(v, pa, pb, fm);
     } else {
       fp_load<G, false>(v, p.dy + ra * p.ldy, hasb ? p.dy + (ra + 1) * p.ldy : nullptr, nullptr, fm);
     }
@@ -892,7 +912,10 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
     static_assert(ONE ? (G::GPC == 2 && 48 * T <= G::BUF_FLOATS + bwd_tm_stash_bytes<LOGN>() / 4)
                       : 48 * T <= G::NBUF * G::BUF_FLOATS,
                   "parking area");
+    // every thread of the group must be past its last exchange read before
+    // the park overwrites the group's buffers (compute-sanitizer racecheck)
     if constexpr (ONE) __syncthreads();
+    else gs.sync();
     float* park = smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS + t;  // [col][T]
     if (c.grp > 0) {
 #pragma unroll
@@ -904,15 +927,11 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
       }
     }
     __syncthreads();
-    if (c.grp > 0) {
-      tmem_fence_before();
-      __syncthreads();
-      tmem_fence_after();
-      if (warp == 0) tmem_dealloc<COLS>(tm_slot);
-      return;
-    }
   }
   float* wsg = p.ws + (int64_t)blockIdx.x * 3 * G::N;
+  // group 0 (whole warps: the TMEM loads are warp-collective) writes the CTA's
+  // partial; every thread then meets at the same barrier before the dealloc
+  if (c.grp == 0) {
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     float ab[8], ad[8], gacc[8];
@@ -939,6 +958,7 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
       wsg[2 * (fm.jsp + s * S)] = gacc[2 * j];
       wsg[2 * (fm.jsp + s * S) + 1] = gacc[2 * j + 1];
     }
+  }
   }
   tmem_fence_before();
   __syncthreads();
@@ -1284,6 +1304,24 @@ static LaunchInfo info_for(int kind) {
   return li;
 }
 
+template <int LOGN>
+static const void* tm_fn() {
+#ifndef ACDC_NO_BWD_TM
+  if constexpr (bwd_tm_ok<LOGN>()) return (const void*)acdc_bwd_tm_kernel<LOGN>;
+#endif
+  return nullptr;
+}
+static const void* tm_kernel_fn(int logn) {
+  switch (logn) {
+    case 9: return tm_fn<9>();
+    case 10: return tm_fn<10>();
+    case 11: return tm_fn<11>();
+    case 12: return tm_fn<12>();
+    case 13: return tm_fn<13>();
+    default: return nullptr;
+  }
+}
+
 static int launch_info(int logn, int kind, LaunchInfo* li) {
   switch (logn) {
 #define ACDC_CASE(L)         \
@@ -1480,7 +1518,7 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
                     const float* h2c, float* grad_a, float* grad_d, float* grad_bias, int accumulate, void* ws,
                     size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, int64_t lddx,
                     acdc_stream_t stream, const int32_t* epi_perm = nullptr, int epi_relu = 0,
-                    const SgdDev* sgd = nullptr) {
+                    const SgdDev* sgd = nullptr, const int32_t* dy_gather = nullptr) {
   if ((kind == K_BWD_H2 || kind == K_BWD_H2_RP) && rows > 0 && !h2c) return ACDC_E_NULL;
   int rc = check_common(x, dx, rows, n, ldx, lddx);
   if (rc) return rc;
@@ -1506,6 +1544,7 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
   p.h2c = const_cast<float*>(h2c);
   p.epi_perm = epi_perm;
   p.epi_relu = epi_relu;
+  p.dy_gather = dy_gather;
 #ifdef ACDC_NO_STAGE
   p.stage = 0;
 #else
@@ -1583,6 +1622,14 @@ int acdc_bwd_cached_f32(const float* x, const float* dy, float* dx, const float*
                   ldx, ldy, lddx, stream);
 }
 
+int cascade_gather_supported(int32_t n) {
+  int logn;
+  if (check_n(n, &logn) || logn < 1) return 0;
+  LaunchInfo li;
+  if (launch_info(logn, K_BWD_H2, &li) || !li.fn) return 0;
+  return li.fn == tm_kernel_fn(logn) ? 1 : 0;
+}
+
 int cascade_bwd_block_f32(const float* x, const float* dy, float* dx, const float* a, const float* d,
                           const float* h2cache, const int32_t* prev_perm, int prev_relu, float* grad_a, float* grad_d,
                           float* grad_bias, int accumulate, void* ws, size_t ws_bytes, int64_t rows, int32_t n,
@@ -1591,6 +1638,21 @@ int cascade_bwd_block_f32(const float* x, const float* dy, float* dx, const floa
   if (prev_perm && dx == dy) return set_error(ACDC_E_SHAPE, "the permuted epilogue cannot write in place");
   return bwd_impl(K_BWD_H2_RP, x, dy, dx, a, d, h2cache, grad_a, grad_d, grad_bias, accumulate, ws, ws_bytes, rows,
                   n, ldx, ldy, lddx, stream, prev_perm, prev_relu);
+}
+
+int cascade_bwd_block_gather_f32(const float* x, const float* dy, float* dx, const float* a, const float* d,
+                                 const float* h2cache, const int32_t* dy_gather, int prev_relu, float* grad_a,
+                                 float* grad_d, float* grad_bias, int accumulate, void* ws, size_t ws_bytes,
+                                 int64_t rows, int32_t n, int64_t ldx, int64_t ldy, int64_t lddx,
+                                 acdc_stream_t stream) {
+  int logn;
+  int rc = check_n(n, &logn);
+  if (rc) return rc;
+  if (acdc_h2cache_bytes(rows, n) == 0 || !cascade_gather_supported(n))
+    return set_error(ACDC_E_SIZE, "the gathered block backward needs the TMEM backward (512 <= n <= 8192)");
+  if (dy_gather && dx == dy) return set_error(ACDC_E_SHAPE, "the gathered block backward cannot write in place");
+  return bwd_impl(K_BWD_H2_RP, x, dy, dx, a, d, h2cache, grad_a, grad_d, grad_bias, accumulate, ws, ws_bytes, rows,
+                  n, ldx, ldy, lddx, stream, nullptr, prev_relu, nullptr, dy_gather);
 }
 
 int acdc_bwd_sgd_f32(const float* x, const float* dy, float* dx, const float* h2cache, const int32_t* prev_perm,

@@ -20,6 +20,7 @@ struct KParams {
   const int* epi_perm;  // bwd epilogue (fused cascade): scatter dx through this permutation
   int epi_relu;         // bwd epilogue: zero dx where x <= 0 (the previous block's ReLU)
   int stage;            // bwd (TMEM kernel): dy rows are 16-byte aligned -> bulk-copy them into smem ahead
+  const int* dy_gather;  // bwd (TMEM kernel, fused cascade): dy[:, i] = dy_in[:, dy_gather[i]] (inverse perm)
   const float2* tab;  // [pass twiddles | c'_k]
   int64_t rows;
   int64_t ldx, ldy, ldo;

@@ -464,7 +464,8 @@ def _ckpt_views(ckpt: torch.Tensor, rows: int, n: int, depth: int):
 
 
 def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor | None, flags,
-                     ckpt: torch.Tensor, grads, accumulate: bool = True, sgd=None, on_block=None) -> torch.Tensor:
+                     ckpt: torch.Tensor, grads, accumulate: bool = True, sgd=None, on_block=None,
+                     perm_inv: torch.Tensor | None = None) -> torch.Tensor:
     """Backward of :func:`cascade_forward` (layers.py:341-344): one cached-h2
     block backward per block, last to first, each applying the previous block's
     ReLU mask and inverse permutation in its epilogue.  ``a``, ``d``: sequences
@@ -474,7 +475,10 @@ def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor
     block's momentum-SGD step is fused into its gradient reduction
     (:func:`acdc_backward_sgd`); the grads are then added in and zeroed.
     ``on_block(l)`` is called after block l's kernels are enqueued (e.g. to
-    start that block's gradient all-reduce while earlier blocks run)."""
+    start that block's gradient all-reduce while earlier blocks run).
+    ``perm_inv`` (argsort of each perm row): where the TMEM backward runs, the
+    permutation after block l is applied as a gather in block l's dy load
+    instead of a scattered store in block l+1's epilogue."""
     depth = len(a)
     n = a[0].shape[0]
     x = _rows2d(x, n)
@@ -496,10 +500,26 @@ def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor
     xs, h2 = _ckpt_views(ckpt, rows, n, depth)
     fl = [int(f) for f in flags]
     lib = _lib.load()
+    gather = sgd is None and perm_inv is not None and lib.cascade_gather_supported(n) == 1
     with torch.cuda.device(dev):
         wsb = lib.acdc_bwd_workspace_bytes(rows, n)
         ws = torch.empty((wsb + 3) // 4, dtype=torch.float32, device=dev)
         for l in range(depth - 1, -1, -1):
+            if gather:  # relu mask in the epilogue, the permutation as this block's dy gather
+                xl = x if l == 0 else xs[l - 1]
+                prev = fl[l - 1] if l > 0 else 0
+                gi = perm_inv[l] if (l < depth - 1 and fl[l] & 2) else None
+                out = torch.empty_like(g)
+                ga, gd, gb = grads[l]
+                al, dl = _vec(a[l], n, dev, "a"), _vec(d[l], n, dev, "d")
+                _lib.check(lib.cascade_bwd_block_gather_f32(
+                    _ptr(xl), _ptr(g), _ptr(out), _ptr(al), _ptr(dl), _ptr(h2[l]), _ptr(gi), 1 if prev & 1 else 0,
+                    _ptr(ga), _ptr(gd), _ptr(gb), 1 if accumulate else 0, _ptr(ws), wsb, rows, n, _ld(xl, n),
+                    _ld(g, n), n, _stream(x)))
+                g = out
+                if on_block is not None:
+                    on_block(l)
+                continue
             xl = x if l == 0 else xs[l - 1]
             prev = fl[l - 1] if l > 0 else 0
             pp = perm[l - 1] if (l > 0 and prev & 2) else None

@@ -418,12 +418,13 @@ class Cascade:
         if any(b[0].device != dev for b in blocks):
             return None
         flags = [(1 if b[1] is not None else 0) | (2 if b[2] is not None else 0) for b in blocks]
-        perm = None
+        perm = perm_inv = None
         if any(f & 2 for f in flags):
             rows = [torch.as_tensor(b[2].perm if b[2] is not None else np.arange(n), dtype=torch.int32) for b in blocks]
             perm = torch.stack(rows).to(dev).contiguous()
+            perm_inv = torch.argsort(perm.long(), dim=1).to(torch.int32).contiguous()
         return {"blocks": blocks, "flags": flags, "flags_t": torch.tensor(flags, dtype=torch.uint8, device=dev),
-                "perm": perm, "n": n, "device": dev}
+                "perm": perm, "perm_inv": perm_inv, "n": n, "device": dev}
 
     @property
     def fused(self) -> bool:
@@ -476,7 +477,7 @@ class Cascade:
             hook = (lambda l: on_layer(acdc[l])) if on_layer is not None else None
             dx = F.cascade_backward(xt, gy, [l.a for l in acdc], [l.d for l in acdc], fz["perm"], fz["flags"], ckpt,
                                     [(l.grad_a, l.grad_d, l.grad_bias_d) for l in acdc], accumulate=True, sgd=sgd,
-                                    on_block=hook)
+                                    on_block=hook, perm_inv=fz["perm_inv"])
             return Layer._out(dx, host)
         g = grad_y
         if host:
