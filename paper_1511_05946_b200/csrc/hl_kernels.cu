@@ -39,7 +39,12 @@
 #include "kernel_common.cuh"
 #include "kparams.h"
 #include "runtime.h"
+#include "tma.cuh"
 #include "tmem.cuh"
+
+#ifndef ACDC_HL_SLOT_DYN
+#define ACDC_HL_SLOT_DYN 0
+#endif
 
 namespace acdc {
 
@@ -50,23 +55,28 @@ struct GeoHL : Geo<LOGN - 1, 0, GPCX> {
   static constexpr int M = B::N;        // complex FFT length
   static constexpr int CPH = M + 1;     // c'_j, j <= N/2
   static constexpr int WNH = M / 2 + 1; // W_N^k, k <= N/4
-  static constexpr int TAB_HL = (2 * (B::TW_ENTRIES + CPH + WNH) + 3) & ~3;  // floats
+  static constexpr int TAB_HL = (2 * (B::TW_ENTRIES + CPH + WNH) + 3) & ~3;  // floats: all tables
+  static constexpr int TAB_TW = (2 * B::TW_ENTRIES + 3) & ~3;                 // floats: pass twiddles only
   static constexpr int SMEM_LIMIT = 227 * 1024;
-  __host__ __device__ static constexpr int by(bool tab, int nbuf) {
-    return 4 * ((tab ? TAB_HL : 0) + B::GPC * nbuf * B::BUF_FLOATS);
-  }
-  static constexpr bool TW_SMEM = by(true, 1) <= SMEM_LIMIT;
-  static constexpr int NBUF = TW_SMEM ? (by(true, 2) <= SMEM_LIMIT ? 2 : 1) : (by(false, 2) <= SMEM_LIMIT ? 2 : 1);
-  static constexpr int TAB_FLOATS = TW_SMEM ? TAB_HL : 0;
+  __host__ __device__ static constexpr int by(int tab, int nbuf) { return 4 * (tab + B::GPC * nbuf * B::BUF_FLOATS); }
+  // all tables in smem if they fit; else the pass twiddles (read by every
+  // butterfly, 32-bit addressing) in smem and c' / W_N (once per slot) in global
+#ifndef ACDC_HL_PREFER_NBUF2  // 1: double-buffered exchanges before c' / W_N in smem (16384: 157 vs 186 KB)
+#define ACDC_HL_PREFER_NBUF2 0
+#endif
+  static constexpr bool CP_SMEM = ACDC_HL_PREFER_NBUF2 ? by(TAB_HL, 2) <= SMEM_LIMIT : by(TAB_HL, 1) <= SMEM_LIMIT;
+  static constexpr bool TW_SMEM = CP_SMEM || by(TAB_TW, 1) <= SMEM_LIMIT;
+  static constexpr int TAB_FLOATS = CP_SMEM ? TAB_HL : (TW_SMEM ? TAB_TW : 0);
+  static constexpr int NBUF = by(TAB_FLOATS, 2) <= SMEM_LIMIT ? 2 : 1;
   static constexpr int GROUP_FLOATS = NBUF * B::BUF_FLOATS;
-  static constexpr int SMEM_BYTES = by(TW_SMEM, NBUF);
+  static constexpr int SMEM_BYTES = by(TAB_FLOATS, NBUF);
   static_assert(B::FP && !B::SPLIT, "the half-length plan runs on the fast-pairing engine");
 };
 
 template <class G>
 __device__ __forceinline__ void stage_tables_hl(const float2* tab, float* smem, const float2*& tw, const float2*& cp,
                                                 const float2*& wn) {
-  constexpr int TOT = G::TW_ENTRIES + G::CPH + G::WNH;
+  constexpr int TOT = G::CP_SMEM ? G::TW_ENTRIES + G::CPH + G::WNH : G::TW_ENTRIES;
   if constexpr (G::TW_SMEM) {
     float2* st = reinterpret_cast<float2*>(smem);
     for (int i = threadIdx.x; i < TOT; i += blockDim.x) st[i] = tab[i];
@@ -75,8 +85,18 @@ __device__ __forceinline__ void stage_tables_hl(const float2* tab, float* smem, 
   } else {
     tw = tab;
   }
-  cp = tw + G::TW_ENTRIES;
+  cp = (G::CP_SMEM ? tw : tab) + G::TW_ENTRIES;
   wn = cp + G::CPH;
+}
+
+// c' / W_N table read: shared memory, or a non-hoistable global load.
+template <class G>
+__device__ __forceinline__ float2 cp_load(const float2* tab, int i) {
+  if constexpr (G::CP_SMEM) {
+    return tab[i];
+  } else {
+    return ldg_f2_volatile(tab + i);
+  }
 }
 
 // Bins of frequency slot s (k = jfq + s*S): {k, N-k, M-k, M+k}; special {0, M, M/2, 3M/2}.
@@ -100,13 +120,13 @@ __device__ __forceinline__ void hl_coefs(const float2* cp, const float2* wn, con
                                          float2& cB, float2& W) {
   const int k = fm.jfq + s * FastMap<G>::S;
   if (fm.special(s)) {
-    cA = tab_load<G>(cp, 0);
-    cB = tab_load<G>(cp, G::M);
-    W = tab_load<G>(cp, G::M / 2);
+    cA = cp_load<G>(cp, 0);
+    cB = cp_load<G>(cp, G::M);
+    W = cp_load<G>(cp, G::M / 2);
   } else {
-    cA = tab_load<G>(cp, k);
-    cB = tab_load<G>(cp, G::M - k);
-    W = tab_load<G>(wn, k);
+    cA = cp_load<G>(cp, k);
+    cB = cp_load<G>(cp, G::M - k);
+    W = cp_load<G>(wn, k);
   }
 }
 
@@ -202,7 +222,11 @@ __global__ void ACDC_LB(GeoHLF<LOGN>) acdc_fwd_hl_kernel(KParams p) {
   constexpr int COLS = hl_fwd_cols<LOGN>();
   pdl_launch_dependents();  // the backward may stage its prologue while this grid drains
   extern __shared__ __align__(16) float smem_f[];
+#if ACDC_HL_SLOT_DYN  // the TMEM address slot after the dynamic shared memory (not at shared address 0)
+  uint32_t& tm_slot = *reinterpret_cast<uint32_t*>(smem_f + G::SMEM_BYTES / 4);
+#else
   __shared__ uint32_t tm_slot;
+#endif
   const auto c = group_ctx<G>();
   const int t = c.t;
   const int warp = threadIdx.x >> 5;
@@ -306,17 +330,31 @@ __global__ void ACDC_LB(GeoHL<LOGN>) acdc_bwd_hl_kernel(KParams p) {
   constexpr bool PRE = T <= 512;  // h2 of the row loaded across the dy transform (register budget)
   pdl_launch_dependents();        // the reduction may launch early; it waits for this grid
   extern __shared__ __align__(16) float smem_f[];
+#if ACDC_HL_SLOT_DYN  // the TMEM address slot after the dynamic shared memory (not at shared address 0)
+  uint32_t& tm_slot = *reinterpret_cast<uint32_t*>(smem_f + G::SMEM_BYTES / 4);
+#else
   __shared__ uint32_t tm_slot;
+#endif
+  __shared__ __align__(8) uint64_t dy_bar[G::GPC];
   const auto c = group_ctx<G>();
   const int t = c.t;
   const int warp = threadIdx.x >> 5;
   GroupSync<G> gs(c.grp);
   Xbuf<G> xb{smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS, 0};
   const FastMap<G> fm(t, gs.mask);
+  // dy staging (double-buffered exchanges, an even number of exchanges per
+  // row): the next row's dy is bulk-copied into exchange buffer A once the
+  // row's last exchange (buffer B) has passed, and read from there next row.
+  constexpr bool STAGE = G::NBUF == 2;  // 2 (NPASS - 1) exchanges per row: the last one is buffer B
+  static_assert(!STAGE || G::NR <= G::BUF_FLOATS, "a dy row fits in one exchange buffer");
+  const bool staged = STAGE && p.stage != 0;
+  float* stg = smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS;
+  uint64_t* bar = &dy_bar[c.grp];
+  if (staged && t == 0) mbar_init(bar, 1);
   if (warp == 0) tmem_alloc<COLS>(&tm_slot);
   tmem_fence_before();
   const float2 *tw, *cp, *wn;
-  stage_tables_hl<G>(p.tab, smem_f, tw, cp, wn);
+  stage_tables_hl<G>(p.tab, smem_f, tw, cp, wn);  // __syncthreads: the barrier init is published
   if constexpr (!G::TW_SMEM) __syncthreads();
   tmem_fence_after();
   // columns: [16 sp, 16 sp + 16) = (b, d) bins of slots 2sp, 2sp+1; [64, 96) grad_a positions (TMA)
@@ -348,6 +386,13 @@ __global__ void ACDC_LB(GeoHL<LOGN>) acdc_bwd_hl_kernel(KParams p) {
     }
   }
   pdl_wait();  // x, dy (maybe the forward's y) and the h2 cache are read from here on
+  auto issue_dy = [&](int64_t row) {  // thread 0 of the group
+    fence_proxy_async_smem();
+    mbar_expect_tx(bar, (uint32_t)G::NR * 4u);
+    bulk_g2s(stg, p.dy + row * p.ldy, (uint32_t)G::NR * 4u, bar);
+  };
+  uint32_t parity = 0;
+  if (staged && t == 0 && c.gid < p.rows) issue_dy(p.rows - 1 - c.gid);
   for (int64_t it = c.gid; it < p.rows; it += c.gstride) {
     const int64_t r = p.rows - 1 - it;  // last-first: the forward's last rows are still in L2
     if (t == 0 && it + c.gstride < p.rows) {
@@ -373,7 +418,23 @@ __global__ void ACDC_LB(GeoHL<LOGN>) acdc_bwd_hl_kernel(KParams p) {
 #pragma unroll
       for (int s = 0; s < 8; ++s) h2v[s] = __ldcs(hc + s * T);
     }
-    hl_load<G, false>(v, p.dy + r * p.ldy, nullptr, fm);
+    if (staged) {
+      mbar_wait(bar, parity);
+      parity ^= 1u;
+      float2 snd[8];
+      const float4* sq = reinterpret_cast<const float4*>(stg) + fm.jsp;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 f = sq[q * S];
+        v[q] = make_float2(f.x, f.z);
+        snd[q] = make_float2(f.w, f.y);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[15 - q] = fm.xor_shfl(snd[q]);
+      gs.sync();  // buffer A is read by every thread before the first exchange writes it
+    } else {
+      hl_load<G, false>(v, p.dy + r * p.ldy, nullptr, fm);
+    }
     fft_passes<G, 0, true>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
     {
       float2 w[8], gl[8], gh[8];
@@ -409,11 +470,15 @@ __global__ void ACDC_LB(GeoHL<LOGN>) acdc_bwd_hl_kernel(KParams p) {
       fp_scatter<G>(gl, gh, v, fm);
     }
     // x of this row: in flight across the g1 transform
-    float4 xv[8];
+    float4 xv[PRE ? 8 : 1];
     const float4* px = reinterpret_cast<const float4*>(p.x + r * p.ldx) + fm.jsp;
+    if constexpr (PRE) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) xv[q] = ld_row_f4(px + q * S);
+      for (int q = 0; q < 8; ++q) xv[q] = ld_row_f4(px + q * S);
+    }
     fft_passes<G, 0, true>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
+    // the row's last exchange (buffer B) has passed: buffer A takes the next dy
+    if (staged && t == 0 && it + c.gstride < p.rows) issue_dy(p.rows - 1 - (it + c.gstride));
     float4 g1[8];
     hl_out<G>(v, g1, fm);
     const float4* pa = reinterpret_cast<const float4*>(p.a) + fm.jsp;
@@ -426,21 +491,22 @@ __global__ void ACDC_LB(GeoHL<LOGN>) acdc_bwd_hl_kernel(KParams p) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int q = 4 * qp + j;
-          acc[4 * j] = fmaf(xv[q].x, g1[q].x, acc[4 * j]);
-          acc[4 * j + 1] = fmaf(xv[q].y, g1[q].y, acc[4 * j + 1]);
-          acc[4 * j + 2] = fmaf(xv[q].z, g1[q].z, acc[4 * j + 2]);
-          acc[4 * j + 3] = fmaf(xv[q].w, g1[q].w, acc[4 * j + 3]);
+          acc[4 * j] = fmaf(xv[PRE ? q : 0].x, g1[q].x, acc[4 * j]);
+          acc[4 * j + 1] = fmaf(xv[PRE ? q : 0].y, g1[q].y, acc[4 * j + 1]);
+          acc[4 * j + 2] = fmaf(xv[PRE ? q : 0].z, g1[q].z, acc[4 * j + 2]);
+          acc[4 * j + 3] = fmaf(xv[PRE ? q : 0].w, g1[q].w, acc[4 * j + 3]);
         }
         tmem_st16f(ta + 64 + 16 * qp, acc);
       }
     } else {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
+        const float4 xq = PRE ? xv[PRE ? q : 0] : ld_row_f4(px + q * S);  // (1024-thread groups: loaded at use)
         float4 gacc = gag[q * S];
-        gacc.x = fmaf(xv[q].x, g1[q].x, gacc.x);
-        gacc.y = fmaf(xv[q].y, g1[q].y, gacc.y);
-        gacc.z = fmaf(xv[q].z, g1[q].z, gacc.z);
-        gacc.w = fmaf(xv[q].w, g1[q].w, gacc.w);
+        gacc.x = fmaf(xq.x, g1[q].x, gacc.x);
+        gacc.y = fmaf(xq.y, g1[q].y, gacc.y);
+        gacc.z = fmaf(xq.z, g1[q].z, gacc.z);
+        gacc.w = fmaf(xq.w, g1[q].w, gacc.w);
         gag[q * S] = gacc;
       }
     }
@@ -487,7 +553,7 @@ template <class K>
 static void geom_hl(LaunchInfo& li) {
   li.cta = K::CTA;
   li.gpc = K::GPC;
-  li.smem = K::SMEM_BYTES;
+  li.smem = K::SMEM_BYTES + (ACDC_HL_SLOT_DYN ? 16 : 0);
   li.unit_rows = 1;
   li.hl = true;
 }
