@@ -62,7 +62,7 @@ struct GeoHL : Geo<LOGN - 1, 0, GPCX> {
   // all tables in smem if they fit; else the pass twiddles (read by every
   // butterfly, 32-bit addressing) in smem and c' / W_N (once per slot) in global
 #ifndef ACDC_HL_PREFER_NBUF2  // 1: double-buffered exchanges before c' / W_N in smem (16384: 157 vs 186 KB)
-#define ACDC_HL_PREFER_NBUF2 0
+#define ACDC_HL_PREFER_NBUF2 1  // A/B at N=16384: -2.9% step (scripts/ab_bench.py, round 2)
 #endif
   static constexpr bool CP_SMEM = ACDC_HL_PREFER_NBUF2 ? by(TAB_HL, 2) <= SMEM_LIMIT : by(TAB_HL, 1) <= SMEM_LIMIT;
   static constexpr bool TW_SMEM = CP_SMEM || by(TAB_TW, 1) <= SMEM_LIMIT;
@@ -345,7 +345,9 @@ __global__ void ACDC_LB(GeoHL<LOGN>) acdc_bwd_hl_kernel(KParams p) {
   // dy staging (double-buffered exchanges, an even number of exchanges per
   // row): the next row's dy is bulk-copied into exchange buffer A once the
   // row's last exchange (buffer B) has passed, and read from there next row.
-  constexpr bool STAGE = G::NBUF == 2;  // 2 (NPASS - 1) exchanges per row: the last one is buffer B
+  // 2 (NPASS - 1) exchanges per row, the last one on buffer B; not with RECOMP
+  // (its extra h2 transform would run through buffer A before dy is read)
+  constexpr bool STAGE = G::NBUF == 2 && !RECOMP;
   static_assert(!STAGE || G::NR <= G::BUF_FLOATS, "a dy row fits in one exchange buffer");
   const bool staged = STAGE && p.stage != 0;
   float* stg = smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS;
