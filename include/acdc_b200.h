@@ -194,6 +194,28 @@ int cascade_bwd_block_gather_f32(const float* x, const float* dy, float* dx, con
                                  int64_t rows, int32_t n, int64_t ldx, int64_t ldy, int64_t lddx,
                                  acdc_stream_t stream);
 
+/* Fused-cascade block backward with the gradient reduction deferred: writes
+ * only the per-CTA gradient partials of block l into ws (a block-private
+ * region of cascade_defer_ws_bytes(rows, n) bytes), so the block-to-block
+ * backward chain does not wait for each block's reduction.  prev_perm
+ * (scatter, as cascade_bwd_block_f32) and dy_gather (gather, as
+ * cascade_bwd_block_gather_f32) are exclusive; prev_relu as for both.
+ * cascade_grad_reduce_f32 then reduces `blocks` such regions (region l at
+ * ws + l * ws_stride_bytes) in one launch, in the same fixed fp64 order as
+ * the per-block reduction: grads is a DEVICE array of 3*blocks float*
+ * ((grad_a, grad_d, grad_bias) of region 0, then region 1, ...), each
+ * stored (=) or accumulated (+=, accumulate != 0).  cascade_defer_ws_bytes
+ * returns 0 where the deferred form does not apply (n outside the fused
+ * cascade's sizes, or more row groups than one reduction pass takes); use the
+ * per-block entry points there. */
+size_t cascade_defer_ws_bytes(int64_t rows, int32_t n);
+int cascade_bwd_block_defer_f32(const float* x, const float* dy, float* dx, const float* a, const float* d,
+                                const float* h2cache, const int32_t* prev_perm, const int32_t* dy_gather,
+                                int prev_relu, void* ws, size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx,
+                                int64_t ldy, int64_t lddx, acdc_stream_t stream);
+int cascade_grad_reduce_f32(const void* ws, size_t ws_stride_bytes, int32_t blocks, int64_t rows, int32_t n,
+                            float* const* grads, int accumulate, acdc_stream_t stream);
+
 /* ---- ReLU and Permutation layers outside the fused cascade (layers.py:218-265) ----
  * acdc_relu_fwd_f32: y = x > 0 ? x : 0 (strict mask, layers.py:227).
  * acdc_relu_bwd_f32: dx = y > 0 ? dy : 0, with y the forward's OUTPUT

@@ -197,8 +197,8 @@ __global__ void ACDC_LB(GeoFwd<LOGN>) acdc_fwd_kernel(KParams p) {
           dct2_post(v[s], w[s], cs, fm.special(s), chi, xl, xh);
           if constexpr (H2C) {
             float4* hc = reinterpret_cast<float4*>(p.h2c + rp * 2 * G::N) + t;  // [slot s][t]
-#ifdef ACDC_H2_KEEP  // normal caching: the tail of the cache stays in L2 for a last-first backward
-            hc[s * G::T] = make_float4(xl.x, xl.y, xh.x, xh.y);
+#ifndef ACDC_H2_STREAM  // normal caching: the tail of the cache stays in L2 for the last-first backward
+            hc[s * G::T] = make_float4(xl.x, xl.y, xh.x, xh.y);  // (evict-first stores measured +0.7% step)
 #else
             __stcs(hc + s * G::T, make_float4(xl.x, xl.y, xh.x, xh.y));
 #endif
@@ -1080,26 +1080,17 @@ struct SgdDev {
   float momentum;
 };
 
-// grad_c[i] (+)= sum_g ws[g][c][i] in double, in a fixed order: block b owns
-// 32 consecutive outputs; warp s sums groups s, s+8, s+16, ... and the 8 warp
-// partials are added in warp order.  Deterministic for a fixed group count.
-// SGD: the reduced gradient feeds the optimizer step instead of being stored
-// (ga/gd/gb, if given, are zeroed like the reference's p.grad[...] = 0).
-template <bool SGD>
-__global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __restrict__ ws, int64_t groups, int n,
-                                                               float* ga, float* gd, float* gb, int accumulate,
-                                                               SgdDev sgd) {
-  // e.g. the next cascade block's backward: its prologue overlaps this.  With
-  // the SGD epilogue the trigger waits for the parameter writes (below): a
-  // dependent backward stages a / d into shared memory before its pdl_wait.
-  if constexpr (!SGD) pdl_launch_dependents();
-  pdl_wait();  // the backward's partials
-  __shared__ double part[8][33];
+// Fixed-order fp64 column sums of one workspace: block b owns 32 consecutive
+// outputs; warp s sums groups s, s+8, s+16, ... and the 8 warp partials are
+// added in warp order.  Returns the sum to warp 0 (idx < total); comp / i name
+// the output (grad_a, grad_d, grad_bias; position).
+__device__ __forceinline__ bool reduce_cols(const float* __restrict__ ws, int64_t groups, int n, double (&part)[8][33],
+                                            double& t, int& comp, int& i) {
   const int o = threadIdx.x & 31, s = threadIdx.x >> 5;
   const int64_t total = 3LL * n;
   const int64_t idx = blockIdx.x * 32LL + o;
   double acc = 0.0;
-  int comp = 0, i = 0;
+  comp = 0, i = 0;
   if (idx < total) {
     comp = (int)(idx / n);
     i = (int)(idx - (int64_t)comp * n);
@@ -1118,10 +1109,30 @@ __global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __re
   }
   part[s][o] = acc;
   __syncthreads();
-  if (s == 0 && idx < total) {
-    double t = 0.0;
+  if (s != 0 || idx >= total) return false;
+  t = 0.0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) t += part[k][o];
+  for (int k = 0; k < 8; ++k) t += part[k][o];
+  return true;
+}
+
+// grad_c[i] (+)= sum_g ws[g][c][i] in double, in a fixed order (reduce_cols).
+// Deterministic for a fixed group count.
+// SGD: the reduced gradient feeds the optimizer step instead of being stored
+// (ga/gd/gb, if given, are zeroed like the reference's p.grad[...] = 0).
+template <bool SGD>
+__global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __restrict__ ws, int64_t groups, int n,
+                                                               float* ga, float* gd, float* gb, int accumulate,
+                                                               SgdDev sgd) {
+  // e.g. the next cascade block's backward: its prologue overlaps this.  With
+  // the SGD epilogue the trigger waits for the parameter writes (below): a
+  // dependent backward stages a / d into shared memory before its pdl_wait.
+  if constexpr (!SGD) pdl_launch_dependents();
+  pdl_wait();  // the backward's partials
+  __shared__ double part[8][33];
+  double t;
+  int comp, i;
+  if (reduce_cols(ws, groups, n, part, t, comp, i)) {
     float* out = comp == 0 ? ga : (comp == 1 ? gd : gb);
     if (accumulate) t += (double)out[i];
     if constexpr (SGD) {
@@ -1140,6 +1151,26 @@ __global__ void __launch_bounds__(256) acdc_grad_reduce_kernel(const float* __re
   if constexpr (SGD) {  // publish the updated parameters, then let the dependent start
     __threadfence();
     pdl_launch_dependents();
+  }
+}
+
+// The same reduction for several cascade blocks in one launch (blockIdx.y =
+// block): block l's partials sit at ws + l * stride, its outputs are
+// grads[3l .. 3l+2].  Takes the per-block reductions off the critical path
+// of the block-to-block backward chain.
+__global__ void __launch_bounds__(256) acdc_grad_reduce_multi_kernel(const float* __restrict__ ws, int64_t stride,
+                                                                     int64_t groups, int n,
+                                                                     float* const* __restrict__ grads,
+                                                                     int accumulate) {
+  pdl_launch_dependents();
+  pdl_wait();  // the last block backward's partials
+  __shared__ double part[8][33];
+  double t;
+  int comp, i;
+  if (reduce_cols(ws + blockIdx.y * stride, groups, n, part, t, comp, i)) {
+    float* out = grads[3 * blockIdx.y + comp];
+    if (accumulate) t += (double)out[i];
+    out[i] = (float)t;
   }
 }
 
@@ -1518,13 +1549,13 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
                     const float* h2c, float* grad_a, float* grad_d, float* grad_bias, int accumulate, void* ws,
                     size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, int64_t lddx,
                     acdc_stream_t stream, const int32_t* epi_perm = nullptr, int epi_relu = 0,
-                    const SgdDev* sgd = nullptr, const int32_t* dy_gather = nullptr) {
+                    const SgdDev* sgd = nullptr, const int32_t* dy_gather = nullptr, bool defer = false) {
   if ((kind == K_BWD_H2 || kind == K_BWD_H2_RP) && rows > 0 && !h2c) return ACDC_E_NULL;
   int rc = check_common(x, dx, rows, n, ldx, lddx);
   if (rc) return rc;
   if (ldy < n) return ACDC_E_SHAPE;
   if (!a || !d || (rows > 0 && !dy)) return ACDC_E_NULL;
-  if (!sgd && (!grad_a || !grad_d || !grad_bias)) return ACDC_E_NULL;
+  if (!sgd && !defer && (!grad_a || !grad_d || !grad_bias)) return ACDC_E_NULL;
   if (accumulate && (!grad_a || !grad_d || !grad_bias)) return ACDC_E_NULL;
   if (!pair_aligned(n, x, ldx) || !pair_aligned(n, dy, ldy) || !pair_aligned(n, dx, lddx) || !pair_aligned(n, a, 0))
     return ACDC_E_ALIGN;
@@ -1575,9 +1606,14 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
     if ((rc = plan_hl(logn, kind, p, &allow))) return rc;
     if ((rc = sized(logn, kind, rows, &li, &grid, allow))) return rc;
     groups = grid * (li.red_per_cta ? li.red_per_cta : li.gpc);
+    if (defer && groups > RED_CHUNK) return set_error(ACDC_E_SIZE, "deferred reduction: too many row groups");
     scratch_floats = li.scratch;
     p.scratch = p.ws + groups * 3 * (int64_t)n;  // scratch follows the partials
     if ((rc = run(kind, p, n, st))) return rc;
+  }
+  if (defer) {  // partials only: cascade_grad_reduce_f32 reduces them later
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
   }
   const int64_t total = 3LL * n;
   int blocks = (int)((total + 31) / 32);
@@ -1653,6 +1689,52 @@ int cascade_bwd_block_gather_f32(const float* x, const float* dy, float* dx, con
   if (dy_gather && dx == dy) return set_error(ACDC_E_SHAPE, "the gathered block backward cannot write in place");
   return bwd_impl(K_BWD_H2_RP, x, dy, dx, a, d, h2cache, grad_a, grad_d, grad_bias, accumulate, ws, ws_bytes, rows,
                   n, ldx, ldy, lddx, stream, nullptr, prev_relu, nullptr, dy_gather);
+}
+
+// Row groups of the block backward (its partials per workspace), or 0 where
+// the deferred reduction does not apply.
+static int64_t defer_groups(int64_t rows, int32_t n) {
+  int logn;
+  if (rows <= 0 || check_n(n, &logn) || acdc_h2cache_bytes(rows, n) == 0) return 0;
+  LaunchInfo li;
+  int64_t grid;
+  if (sized(logn, K_BWD_H2_RP, rows, &li, &grid, true)) return 0;
+  const int64_t groups = grid * (li.red_per_cta ? li.red_per_cta : li.gpc);
+  return groups <= RED_CHUNK ? groups : 0;
+}
+
+size_t cascade_defer_ws_bytes(int64_t rows, int32_t n) {
+  if (defer_groups(rows, n) == 0) return 0;
+  const size_t b = acdc_bwd_workspace_bytes(rows, n);
+  return (b + 255) & ~(size_t)255;
+}
+
+int cascade_bwd_block_defer_f32(const float* x, const float* dy, float* dx, const float* a, const float* d,
+                                const float* h2cache, const int32_t* prev_perm, const int32_t* dy_gather,
+                                int prev_relu, void* ws, size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx,
+                                int64_t ldy, int64_t lddx, acdc_stream_t stream) {
+  if (rows > 0 && defer_groups(rows, n) == 0)
+    return set_error(ACDC_E_SIZE, "deferred reduction: unsupported size (see cascade_defer_ws_bytes)");
+  if (prev_perm && dy_gather) return set_error(ACDC_E_SHAPE, "prev_perm and dy_gather are exclusive");
+  if (dy_gather && !cascade_gather_supported(n))
+    return set_error(ACDC_E_SIZE, "the gathered block backward needs the TMEM backward (512 <= n <= 8192)");
+  if ((prev_perm || dy_gather) && dx == dy) return set_error(ACDC_E_SHAPE, "the permuted block backward cannot write in place");
+  return bwd_impl(K_BWD_H2_RP, x, dy, dx, a, d, h2cache, nullptr, nullptr, nullptr, 0, ws, ws_bytes, rows, n, ldx,
+                  ldy, lddx, stream, prev_perm, prev_relu, nullptr, dy_gather, true);
+}
+
+int cascade_grad_reduce_f32(const void* ws, size_t ws_stride_bytes, int32_t blocks, int64_t rows, int32_t n,
+                            float* const* grads, int accumulate, acdc_stream_t stream) {
+  if (blocks <= 0 || rows <= 0) return blocks < 0 || rows < 0 ? ACDC_E_SHAPE : ACDC_OK;
+  const int64_t groups = defer_groups(rows, n);
+  if (groups == 0) return set_error(ACDC_E_SIZE, "deferred reduction: unsupported size (see cascade_defer_ws_bytes)");
+  if (!ws || !grads) return ACDC_E_NULL;
+  if (ws_stride_bytes % sizeof(float) || ws_stride_bytes < acdc_bwd_workspace_bytes(rows, n)) return ACDC_E_WS;
+  const int blocks_x = (int)((3LL * n + 31) / 32);
+  launch_pdl(acdc_grad_reduce_multi_kernel, dim3(blocks_x, blocks), (cudaStream_t)stream, (const float*)ws,
+             (int64_t)(ws_stride_bytes / sizeof(float)), groups, n, grads, accumulate);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
 }
 
 int acdc_bwd_sgd_f32(const float* x, const float* dy, float* dx, const float* h2cache, const int32_t* prev_perm,

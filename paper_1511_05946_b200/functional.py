@@ -501,6 +501,14 @@ def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor
     fl = [int(f) for f in flags]
     lib = _lib.load()
     gather = sgd is None and perm_inv is not None and lib.cascade_gather_supported(n) == 1
+    # Without a per-block hook or fused SGD, every block writes only its
+    # gradient partials and one launch reduces all blocks at the end: the
+    # block-to-block chain no longer waits for a reduction per block.
+    dstride = lib.cascade_defer_ws_bytes(rows, n) if (sgd is None and on_block is None) else 0
+    tab = _grad_table(grads, dev) if dstride else None
+    if tab is not None:
+        return _cascade_backward_deferred(x, g, a, d, perm, fl, xs, h2, grads, tab, accumulate,
+                                          perm_inv if gather else None, dstride)
     with torch.cuda.device(dev):
         wsb = lib.acdc_bwd_workspace_bytes(rows, n)
         ws = torch.empty((wsb + 3) // 4, dtype=torch.float32, device=dev)
@@ -541,6 +549,57 @@ def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor
             g = out
             if on_block is not None:
                 on_block(l)
+    return g
+
+
+_grad_tables: dict = {}
+
+
+def _grad_table(grads, dev) -> torch.Tensor:
+    """Device array of the blocks' (grad_a, grad_d, grad_bias) pointers, cached
+    per pointer tuple (the layers' gradient buffers are persistent)."""
+    for gr in grads:
+        for t in gr:
+            if t.device != dev or t.dtype != torch.float32 or not t.is_contiguous() or t.dim() != 1:
+                raise ValueError("gradient buffers must be contiguous fp32 (n,) tensors on the input device")
+    key = (dev.index, tuple(t.data_ptr() for gr in grads for t in gr))
+    tab = _grad_tables.get(key)
+    if tab is None:
+        if torch.cuda.is_current_stream_capturing():
+            return None  # no host-to-device copy inside a capture: the caller uses the per-block reductions
+        if len(_grad_tables) > 64:
+            _grad_tables.clear()
+        tab = torch.tensor(key[1], dtype=torch.int64).to(dev)
+        _grad_tables[key] = tab
+    return tab
+
+
+def _cascade_backward_deferred(x, g, a, d, perm, fl, xs, h2, grads, tab, accumulate, perm_inv, stride):
+    depth = len(a)
+    n = a[0].shape[0]
+    rows = x.shape[0]
+    dev = x.device
+    lib = _lib.load()
+    if any(t.shape != (n,) for gr in grads for t in gr):
+        raise ValueError("gradient buffers must be contiguous fp32 (n,) tensors on the input device")
+    with torch.cuda.device(dev):
+        ws = torch.empty(depth * stride // 4, dtype=torch.float32, device=dev)
+        for l in range(depth - 1, -1, -1):
+            xl = x if l == 0 else xs[l - 1]
+            prev = fl[l - 1] if l > 0 else 0
+            if perm_inv is not None:  # the permutation after block l as this block's dy gather
+                pp, gi = None, (perm_inv[l] if (l < depth - 1 and fl[l] & 2) else None)
+            else:  # the permutation before block l as a scatter in its epilogue
+                pp, gi = (perm[l - 1] if (l > 0 and prev & 2) else None), None
+            out = torch.empty_like(g)
+            al, dl = _vec(a[l], n, dev, "a"), _vec(d[l], n, dev, "d")
+            _lib.check(lib.cascade_bwd_block_defer_f32(
+                _ptr(xl), _ptr(g), _ptr(out), _ptr(al), _ptr(dl), _ptr(h2[l]), _ptr(pp), _ptr(gi),
+                1 if prev & 1 else 0, ws.data_ptr() + l * stride, stride, rows, n, _ld(xl, n), _ld(g, n), n,
+                _stream(x)))
+            g = out
+        _lib.check(lib.cascade_grad_reduce_f32(_ptr(ws), stride, depth, rows, n, _ptr(tab), 1 if accumulate else 0,
+                                               _stream(x)))
     return g
 
 

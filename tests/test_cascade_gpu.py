@@ -143,3 +143,42 @@ def test_fused_matches_unfused():
     torch.testing.assert_close(dx1, dx2, rtol=1e-4, atol=1e-4)
     for u, v in zip(g1, g2):
         torch.testing.assert_close(u, v, rtol=1e-4, atol=1e-3)
+
+
+@pytest.mark.parametrize("n,depth,rows,relu,perm", [(256, 3, 9, True, True), (1024, 12, 130, True, True),
+                                                    (2048, 4, 64, False, True), (4096, 3, 40, True, False)])
+def test_deferred_reduction_matches_per_block(n, depth, rows, relu, perm):
+    """The deferred form (block partials, one multi-block reduction at the end)
+    is bit-identical to one reduction per block (forced by a per-layer hook),
+    with accumulation into existing gradients, for the scatter (n=256) and the
+    gather (512 <= n <= 8192) epilogues."""
+    from paper_1511_05946_b200 import _lib
+
+    rng = np.random.default_rng(7)
+    casc, layers, _ = build(n, depth, rng, relu=relu, perm=perm)
+    assert casc._fused is not None
+    assert _lib.load().cascade_defer_ws_bytes(rows, n) > 0
+    x = torch.as_tensor(f32(rng, rows, n), device=DEV)
+    dy = torch.as_tensor(f32(rng, rows, n), device=DEV)
+    acdc = [L for L in layers if hasattr(L, "grad_a")]
+    res = []
+    for hook in (None, lambda layer: None):
+        for L in acdc:  # accumulate onto a nonzero starting gradient
+            for g in (L.grad_a, L.grad_d, L.grad_bias_d):
+                g.fill_(0.25)
+        casc.forward(x)
+        dx = casc.backward(dy, on_layer=hook)
+        torch.cuda.synchronize()
+        res.append([dx.clone()] + [g.clone() for L in acdc for g in (L.grad_a, L.grad_d, L.grad_bias_d)])
+    for a_, b_ in zip(*res):
+        assert torch.equal(a_, b_)
+
+
+def test_deferred_reduction_abi_errors():
+    from paper_1511_05946_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.cascade_defer_ws_bytes(64, 128) == 0  # below the fused cascade's sizes
+    assert lib.cascade_defer_ws_bytes(0, 1024) == 0
+    assert lib.cascade_grad_reduce_f32(None, 0, 0, 0, 1024, None, 0, None) == 0  # nothing to reduce
+    assert lib.cascade_grad_reduce_f32(None, 1 << 20, 2, 64, 1000, None, 0, None) != 0  # not a power of two
