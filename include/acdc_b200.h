@@ -216,6 +216,24 @@ int cascade_bwd_block_defer_f32(const float* x, const float* dy, float* dx, cons
 int cascade_grad_reduce_f32(const void* ws, size_t ws_stride_bytes, int32_t blocks, int64_t rows, int32_t n,
                             float* const* grads, int accumulate, acdc_stream_t stream);
 
+/* Two consecutive fused-cascade blocks in one launch, deferred reduction:
+ * block hi = l+1 (x_hi = x_{l+1}, h2_hi, a_hi, d_hi; dy gathered through
+ * dy_gather_hi as in cascade_bwd_block_gather_f32; dx masked by relu_hi = the
+ * ReLU after block l) then block lo = l on the same rows, whose dy is block
+ * hi's dx kept on chip (gathered through dy_gather_lo = argsort of the
+ * permutation after block l, or NULL) and whose dx is masked by relu_lo and
+ * written to dx.  Partials go to ws_hi / ws_lo (block-private regions of
+ * cascade_defer_ws_bytes bytes each) for cascade_grad_reduce_f32.  Only where
+ * cascade_pair_supported(rows, n) != 0 (the TMEM backward sizes whose two-block
+ * form fits on chip with both blocks' parameter stashes, 512 <= n <= 2048). */
+int cascade_pair_supported(int64_t rows, int32_t n);
+int cascade_bwd_pair_defer_f32(const float* x_hi, const float* x_lo, const float* dy, float* dx, const float* a_hi,
+                               const float* d_hi, const float* a_lo, const float* d_lo, const float* h2_hi,
+                               const float* h2_lo, const int32_t* dy_gather_hi, const int32_t* dy_gather_lo,
+                               int relu_hi, int relu_lo, void* ws_hi, void* ws_lo, size_t ws_bytes, int64_t rows,
+                               int32_t n, int64_t ldx_hi, int64_t ldx_lo, int64_t ldy, int64_t lddx,
+                               acdc_stream_t stream);
+
 /* ---- ReLU and Permutation layers outside the fused cascade (layers.py:218-265) ----
  * acdc_relu_fwd_f32: y = x > 0 ? x : 0 (strict mask, layers.py:227).
  * acdc_relu_bwd_f32: dx = y > 0 ? dy : 0, with y the forward's OUTPUT

@@ -94,6 +94,12 @@ SIGNATURES = {
         [_P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _I64, _I32, _I64, _I64, _I64, _P],
     ),
     "cascade_grad_reduce_f32": (ctypes.c_int, [_P, ctypes.c_size_t, _I32, _I64, _I32, _P, ctypes.c_int, _P]),
+    "cascade_pair_supported": (ctypes.c_int, [_I64, _I32]),
+    "cascade_bwd_pair_defer_f32": (
+        ctypes.c_int,
+        [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int, ctypes.c_int, _P, _P, ctypes.c_size_t, _I64,
+         _I32, _I64, _I64, _I64, _I64, _P],
+    ),
     "acdc_relu_fwd_f32": (ctypes.c_int, [_P, _P, _I64, _I32, _I64, _I64, _P]),
     "acdc_relu_bwd_f32": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I64, _I64, _I64, _P]),
     "acdc_gather_cols": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _I64, _I64, _P]),

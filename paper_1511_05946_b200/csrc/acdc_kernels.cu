@@ -966,6 +966,319 @@ __global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm_kernel(KParams p) {
   if (warp == 0) tmem_dealloc<COLS>(tm_slot);
 }
 
+// Fused-cascade backward of TWO consecutive blocks per launch (Cascade.backward,
+// layers.py:341-344): block hi = l+1 (operands in p.x / a / d / h2c /
+// dy_gather / epi_relu / ws) and then block lo = l (p.x2 / a2 / d2 / h2c2 /
+// dy_gather2 / epi_relu2 / ws2) on the same row pair, with block hi's dx kept
+// on chip: its epilogue writes the masked rows into exchange buffer A (idle
+// after the g1 transform's last exchange) and block lo reads its dy from there
+// (through its inverse permutation), so the dx / dy round trip through HBM and
+// one launch per block pair disappear.  Per-block gradient partials as in
+// acdc_bwd_tm_kernel (96 TMEM columns per thread: [0,48) block hi, [48,96)
+// block lo); both are written to their block-private workspaces and reduced
+// later by acdc_grad_reduce_multi_kernel (deferred form only).
+template <int LOGN>
+__host__ __device__ constexpr bool bwd_tm2_astash() {
+  using G = GeoBwdTm<LOGN>;
+  return G::SMEM_BYTES + 4 * 8 * G::T * 8 <= G::SMEM_LIMIT;
+}
+template <int LOGN>
+__host__ __device__ constexpr int bwd_tm2_stash_bytes() {
+  using G = GeoBwdTm<LOGN>;
+  return (bwd_tm2_astash<LOGN>() ? 4 : 2) * 8 * G::T * 8;
+}
+template <int LOGN>
+__host__ __device__ constexpr bool bwd_tm2_ok() {
+  using G = GeoBwdTm<LOGN>;
+  // N <= 2048: at N = 4096 the four stashes leave almost no L1 (the one-block kernel is sensitive to
+  // that) and C4 measured +0.4% against one block per launch
+  return bwd_tm_ok<LOGN>() && LOGN <= 11 && G::NBUF == 2 && bwd_tm2_astash<LOGN>() &&
+         G::SMEM_BYTES + bwd_tm2_stash_bytes<LOGN>() <= G::SMEM_LIMIT &&
+         (G::CTA / 32 / 4) * 96 <= 512 && 48 * G::T <= G::NBUF * G::BUF_FLOATS;
+}
+template <int LOGN>
+__host__ __device__ constexpr int bwd_tm2_cols() {
+  using G = GeoBwdTm<LOGN>;
+  constexpr int need = (G::CTA / 32 / 4) * 96;
+  return need <= 128 ? 128 : need <= 256 ? 256 : 512;
+}
+
+template <int LOGN>
+__global__ void ACDC_LB(GeoBwdTm<LOGN>) acdc_bwd_tm2_kernel(KParams p) {
+  using G = GeoBwdTm<LOGN>;
+  pdl_launch_dependents();
+  constexpr int T = G::T;
+  constexpr int S = FastMap<G>::S;
+  constexpr int COLS = bwd_tm2_cols<LOGN>();
+  constexpr bool AST = bwd_tm2_astash<LOGN>();
+  static_assert(bwd_tm2_ok<LOGN>(), "two-block TMEM backward does not fit at this size");
+  extern __shared__ __align__(16) float smem_f[];
+  __shared__ uint32_t tm_slot;
+  __shared__ __align__(8) uint64_t dy_bar[G::GPC];
+  const auto c = group_ctx<G>();
+  const int t = c.t;
+  const int warp = threadIdx.x >> 5;
+  GroupSync<G> gs(c.grp);
+  Xbuf<G> xb{smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS, 0};
+  float* stg = smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS;  // exchange buffer A
+  uint64_t* bar = &dy_bar[c.grp];
+  const bool staged = p.stage != 0;
+  if (staged && t == 0) mbar_init(bar, 1);
+  // stashes [blk][s][t]: d pairs (blk 0, 1), then a pairs (blk 0, 1) where they fit
+  float2* dst_all = reinterpret_cast<float2*>(smem_f + G::SMEM_BYTES / 4);
+  const FastMap<G> fm(t, gs.mask);
+  if (c.grp == 0) {
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      dst_all[t + s * T] = make_float2(__ldg(fm.plo(p.d, s)), __ldg(fm.phi(p.d, s)));
+      dst_all[8 * T + t + s * T] = make_float2(__ldg(fm.plo(p.d2, s)), __ldg(fm.phi(p.d2, s)));
+      if constexpr (AST) {
+        dst_all[16 * T + t + s * T] = ld_f2(p.a + 2 * (fm.jsp + s * S));
+        dst_all[24 * T + t + s * T] = ld_f2(p.a2 + 2 * (fm.jsp + s * S));
+      }
+    }
+  }
+  if (warp == 0) tmem_alloc<COLS>(&tm_slot);
+  tmem_fence_before();
+  const float2 *tw, *cp;
+  stage_tables<G>(p.tab, smem_f, tw, cp);
+  if constexpr (!G::TW_SMEM) __syncthreads();
+  tmem_fence_after();
+  // columns of this thread: block hi [0,48), block lo [48,96); each [0,16) grad_bias bins,
+  // [16,32) grad_d bins, [32,48) grad_a positions
+  const uint32_t tbase = tmem_addr(tm_slot, warp, (warp >> 2) * 96);
+  {
+    float z[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) z[i] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) tmem_st8(tbase + 8 * k, z);
+  }
+  const int64_t npairs = (p.rows + 1) >> 1;
+  const float2 chi = tab_load<G>(cp, G::N / 2);
+  auto issue_dy = [&](int64_t r) {
+    const bool hb = 2 * r + 1 < p.rows;
+    const uint32_t rowb = (uint32_t)G::N * 4u;
+    fence_proxy_async_smem();
+    mbar_expect_tx(bar, hb ? 2u * rowb : rowb);
+    bulk_g2s(stg, p.dy + 2 * r * p.ldy, rowb, bar);
+    if (hb) bulk_g2s(stg + G::N, p.dy + (2 * r + 1) * p.ldy, rowb, bar);
+  };
+  uint32_t parity = 0;
+  auto rmap = [&](int64_t i) { return ACDC_BWD_REV ? npairs - 1 - i : i; };
+  pdl_wait();
+  if (staged && t == 0 && c.gid < npairs) issue_dy(rmap(c.gid));
+  for (int64_t it = c.gid; it < npairs; it += c.gstride) {
+    const int64_t rp = rmap(it);
+    const int64_t ra = 2 * rp;
+    const bool hasb = ra + 1 < p.rows;
+    const int64_t rb = hasb ? ra + 1 : ra;
+    if (t == 0 && it + ACDC_PF_DIST * c.gstride < npairs) {
+      const int64_t nr = 2 * rmap(it + ACDC_PF_DIST * c.gstride);
+      prefetch_row_l2(p.dy + nr * p.ldy, G::N);
+      prefetch_row_l2(p.x + nr * p.ldx, G::N);
+      prefetch_row_l2(p.x2 + nr * p.ldx2, G::N);
+      if (nr + 1 < p.rows) {
+        prefetch_row_l2(p.dy + (nr + 1) * p.ldy, G::N);
+        prefetch_row_l2(p.x + (nr + 1) * p.ldx, G::N);
+        prefetch_row_l2(p.x2 + (nr + 1) * p.ldx2, G::N);
+      }
+    }
+#pragma unroll 1
+    for (int blk = 0; blk < 2; ++blk) {
+      const uint32_t ta = tbase + 48 * blk;
+      const float* bx = blk ? p.x2 : p.x;
+      const int64_t bldx = blk ? p.ldx2 : p.ldx;
+      const float* bh2 = blk ? p.h2c2 : p.h2c;
+      const int* bgat = blk ? p.dy_gather2 : p.dy_gather;
+      const int brelu = blk ? p.epi_relu2 : p.epi_relu;
+      const float* ba = blk ? p.a2 : p.a;
+      const float2* dst = dst_all + 8 * T * blk + t;
+      const float2* ast = dst_all + 16 * T + 8 * T * blk + t;
+      const float4* hc = reinterpret_cast<const float4*>(bh2 + rp * 2 * G::N) + t;
+      float4 h2v[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) h2v[s] = __ldcs(hc + s * T);
+      float2 v[16];
+      if (blk == 1 || staged) {  // dy rows in buffer A: block lo's from block hi's epilogue, block hi's by TMA
+        if (blk == 0) {
+          mbar_wait(bar, parity);
+          parity ^= 1u;
+        } else {
+          gs.sync();  // block hi's epilogue writes are visible to the group
+        }
+        float2 pa[8], pb[8];
+        if (bgat) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int2 iv = __ldg(reinterpret_cast<const int2*>(bgat) + fm.jsp + q * S);
+            pa[q] = make_float2(stg[iv.x], stg[iv.y]);
+            pb[q] = hasb ? make_float2(stg[G::N + iv.x], stg[G::N + iv.y]) : make_float2(0.f, 0.f);
+          }
+        } else {
+          const float2* sa = reinterpret_cast<const float2*>(stg) + fm.jsp;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            pa[q] = sa[q * S];
+            pb[q] = hasb ? sa[G::N / 2 + q * S] : make_float2(0.f, 0.f);
+          }
+        }
+        fp_from_pairs<G>(v, pa, pb, fm);
+        gs.sync();  // buffer A is read by every thread before exchange 1 writes it
+      } else if (bgat) {
+        float2 pa[8], pb[8];
+        const float* ya = p.dy + ra * p.ldy;
+        const float* yb = p.dy + rb * p.ldy;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int2 iv = __ldg(reinterpret_cast<const int2*>(bgat) + fm.jsp + q * S);
+          pa[q] = make_float2(__ldg(ya + iv.x), __ldg(ya + iv.y));
+          pb[q] = hasb ? make_float2(__ldg(yb + iv.x), __ldg(yb + iv.y)) : make_float2(0.f, 0.f);
+        }
+        fp_from_pairs<G>(v, pa, pb, fm);
+      } else {
+        fp_load<G, false>(v, p.dy + ra * p.ldy, hasb ? p.dy + (ra + 1) * p.ldy : nullptr, nullptr, fm);
+      }
+      fft_passes<G, 0, ACDC_TM_LATE_PAD1>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
+      {
+        float2 w[8], gl[8], gh[8];
+        fp_partner<G>(v, w, fm);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          float ab[8], ad[8];
+          tmem_ld8(ta + 8 * half, ab);
+          tmem_ld8(ta + 16 + 8 * half, ad);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int s = 4 * half + j;
+            const float2 cs = tab_load<G>(fm.plo(cp, s), 0);
+            float2 g3l, g3h;
+            dct2_post(v[s], w[s], cs, fm.special(s), chi, g3l, g3h);
+            ab[2 * j] += g3l.x + g3l.y;
+            ab[2 * j + 1] += g3h.x + g3h.y;
+            const float4 h4 = h2v[s];
+            ad[2 * j] = fmaf(h4.x, g3l.x, fmaf(h4.y, g3l.y, ad[2 * j]));
+            ad[2 * j + 1] = fmaf(h4.z, g3h.x, fmaf(h4.w, g3h.y, ad[2 * j + 1]));
+            const float2 dv = dst[s * T];
+            dct3_pre(vmul(bc(dv.x), g3l), vmul(bc(dv.y), g3h), cs, fm.special(s), chi, gl[s], gh[s]);
+          }
+          tmem_st8(ta + 8 * half, ab);
+          tmem_st8(ta + 16 + 8 * half, ad);
+        }
+        fp_scatter<G>(gl, gh, v, fm);
+      }
+      float2 xav[8], xbv[8];
+      {
+        const float* pxa = bx + ra * bldx + 2 * fm.jsp;
+        const float* pxb = bx + rb * bldx + 2 * fm.jsp;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          xav[q] = ld_row_f2(pxa + 2 * q * S);
+          xbv[q] = ld_row_f2(pxb + 2 * q * S);
+        }
+      }
+      fft_passes<G, 0, ACDC_TM_LATE_PAD2>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
+      // exchange 4 has passed: buffer A takes block hi's dx, or (after block lo) the next dy
+      if (blk == 1 && staged && t == 0 && it + c.gstride < npairs) issue_dy(rmap(it + c.gstride));
+      float2 ga[8], gb[8];
+      fp_out_pairs<G>(v, ga, gb, fm);
+      {
+        float gacc[8];
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          tmem_ld8(ta + 32 + 8 * half, gacc);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int q = 4 * half + j;
+            if (!hasb) xbv[q] = make_float2(0.f, 0.f);
+            const float2 gsum = cadd(make_float2(gacc[2 * j], gacc[2 * j + 1]),
+                                     vfma(gb[q], xbv[q], vmul(ga[q], xav[q])));
+            gacc[2 * j] = gsum.x;
+            gacc[2 * j + 1] = gsum.y;
+            const float2 av = AST ? ast[q * T] : ld_f2(ba + 2 * (fm.jsp + q * S));
+            float2 da = vmul(av, ga[q]);
+            float2 db = vmul(av, gb[q]);
+            if (brelu) {  // previous block's ReLU: mask = x > 0 (layers.py:227, 233)
+              da = make_float2(xav[q].x > 0.f ? da.x : 0.f, xav[q].y > 0.f ? da.y : 0.f);
+              db = make_float2(xbv[q].x > 0.f ? db.x : 0.f, xbv[q].y > 0.f ? db.y : 0.f);
+            }
+            ga[q] = da;
+            gb[q] = db;
+          }
+          tmem_st8(ta + 32 + 8 * half, gacc);
+        }
+      }
+      if (blk == 0) {  // block hi's dx rows -> buffer A (natural layout), block lo's dy
+        float2* sa = reinterpret_cast<float2*>(stg) + fm.jsp;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          sa[q * S] = ga[q];
+          if (hasb) sa[G::N / 2 + q * S] = gb[q];
+        }
+      } else {
+        float2* oa = reinterpret_cast<float2*>(p.y + ra * p.ldo + 2 * fm.jsp);
+        float2* ob = reinterpret_cast<float2*>(p.y + rb * p.ldo + 2 * fm.jsp);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          st_row_f2(oa + q * S, ga[q]);
+          if (hasb) st_row_f2(ob + q * S, gb[q]);
+        }
+      }
+    }
+  }
+  // Per block: one partial per CTA (groups 1.. park their 48 columns, group 0 adds them in order).
+#pragma unroll 1
+  for (int blk = 0; blk < 2; ++blk) {
+    const uint32_t ta = tbase + 48 * blk;
+    __syncthreads();  // last exchange reads / previous block's park reads are done
+    float* park = smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS + t;  // [col][T]
+    if (c.grp > 0) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        float u[8];
+        tmem_ld8(ta + 8 * k, u);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) park[(8 * k + i) * T] = u[i];
+      }
+    }
+    __syncthreads();
+    float* wsg = (blk ? p.ws2 : p.ws) + (int64_t)blockIdx.x * 3 * G::N;
+    if (c.grp == 0) {
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        float ab[8], ad[8], gacc[8];
+        tmem_ld8(ta + 8 * half, ab);
+        tmem_ld8(ta + 16 + 8 * half, ad);
+        tmem_ld8(ta + 32 + 8 * half, gacc);
+#pragma unroll
+        for (int g = 1; g < G::GPC; ++g) {
+          const float* pk = smem_f + G::TAB_FLOATS + g * G::GROUP_FLOATS + t;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            ab[i] += pk[(8 * half + i) * T];
+            ad[i] += pk[(16 + 8 * half + i) * T];
+            gacc[i] += pk[(32 + 8 * half + i) * T];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int s = 4 * half + j;
+          *fm.plo(wsg + 2 * G::N, s) = ab[2 * j];
+          *fm.phi(wsg + 2 * G::N, s) = ab[2 * j + 1];
+          *fm.plo(wsg + G::N, s) = ad[2 * j];
+          *fm.phi(wsg + G::N, s) = ad[2 * j + 1];
+          wsg[2 * (fm.jsp + s * S)] = gacc[2 * j];
+          wsg[2 * (fm.jsp + s * S) + 1] = gacc[2 * j + 1];
+        }
+      }
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  if (warp == 0) tmem_dealloc<COLS>(tm_slot);
+}
+
 // Row-wise orthonormal DCT-II (transforms.py:137-145) / DCT-III (148-156).
 template <int LOGN>
 __global__ void ACDC_LB(Geo<LOGN>) acdc_dct2_kernel(KParams p) {
@@ -1353,6 +1666,40 @@ static const void* tm_kernel_fn(int logn) {
   }
 }
 
+// Two-block cascade backward (acdc_bwd_tm2_kernel): launch description, or
+// fn == nullptr where it does not fit.
+template <int LOGN>
+static LaunchInfo tm2_info() {
+  LaunchInfo li;
+#ifndef ACDC_NO_BWD_TM
+  if constexpr (bwd_tm2_ok<LOGN>()) {
+    li.fn = (const void*)acdc_bwd_tm2_kernel<LOGN>;
+    geom<GeoBwdTm<LOGN>>(li, 0);
+    li.red_per_cta = 1;
+#ifndef ACDC_NO_PDL
+    li.pdl = true;
+#endif
+    li.smem += bwd_tm2_stash_bytes<LOGN>();
+    li.max_per_sm = 512 / bwd_tm2_cols<LOGN>();
+  }
+#endif
+  return li;
+}
+static LaunchInfo tm2_launch_info(int logn) {
+  switch (logn) {
+#ifndef ACDC_ONLY_LOGN
+    case 9: return tm2_info<9>();
+    case 10: return tm2_info<10>();
+    case 11: return tm2_info<11>();
+    case 12: return tm2_info<12>();
+    case 13: return tm2_info<13>();
+#elif ACDC_ONLY_LOGN >= 9 && ACDC_ONLY_LOGN <= 13
+    case ACDC_ONLY_LOGN: return tm2_info<ACDC_ONLY_LOGN>();
+#endif
+    default: return LaunchInfo{};
+  }
+}
+
 static int launch_info(int logn, int kind, LaunchInfo* li) {
   switch (logn) {
 #define ACDC_CASE(L)         \
@@ -1721,6 +2068,75 @@ int cascade_bwd_block_defer_f32(const float* x, const float* dy, float* dx, cons
   if ((prev_perm || dy_gather) && dx == dy) return set_error(ACDC_E_SHAPE, "the permuted block backward cannot write in place");
   return bwd_impl(K_BWD_H2_RP, x, dy, dx, a, d, h2cache, nullptr, nullptr, nullptr, 0, ws, ws_bytes, rows, n, ldx,
                   ldy, lddx, stream, prev_perm, prev_relu, nullptr, dy_gather, true);
+}
+
+int cascade_pair_supported(int64_t rows, int32_t n) {
+  int logn;
+  if (rows <= 0 || check_n(n, &logn) || defer_groups(rows, n) == 0) return 0;
+  const LaunchInfo li = tm2_launch_info(logn);
+  if (!li.fn) return 0;
+  LaunchInfo l1;
+  int64_t g1, g2;
+  if (sized(logn, K_BWD_H2_RP, rows, &l1, &g1, true) || grid_for(li, (rows + 1) / 2, &g2)) return 0;
+  return g1 == g2 ? 1 : 0;  // same CTAs -> same partial layout as the one-block form
+}
+
+int cascade_bwd_pair_defer_f32(const float* x_hi, const float* x_lo, const float* dy, float* dx, const float* a_hi,
+                               const float* d_hi, const float* a_lo, const float* d_lo, const float* h2_hi,
+                               const float* h2_lo, const int32_t* dy_gather_hi, const int32_t* dy_gather_lo,
+                               int relu_hi, int relu_lo, void* ws_hi, void* ws_lo, size_t ws_bytes, int64_t rows,
+                               int32_t n, int64_t ldx_hi, int64_t ldx_lo, int64_t ldy, int64_t lddx,
+                               acdc_stream_t stream) {
+  if (rows == 0) return ACDC_OK;
+  if (rows < 0) return ACDC_E_SHAPE;
+  if (!cascade_pair_supported(rows, n))
+    return set_error(ACDC_E_SIZE, "two-block cascade backward: unsupported size (see cascade_pair_supported)");
+  if (!x_hi || !x_lo || !dy || !dx || !a_hi || !d_hi || !a_lo || !d_lo || !h2_hi || !h2_lo || !ws_hi || !ws_lo)
+    return ACDC_E_NULL;
+  if (ldx_hi < n || ldx_lo < n || ldy < n || lddx < n) return ACDC_E_SHAPE;
+  if (dx == dy) return set_error(ACDC_E_SHAPE, "the two-block backward cannot write in place");
+  if (!pair_aligned(n, x_hi, ldx_hi) || !pair_aligned(n, x_lo, ldx_lo) || !pair_aligned(n, dy, ldy) ||
+      !pair_aligned(n, dx, lddx) || !pair_aligned(n, a_hi, 0) || !pair_aligned(n, a_lo, 0))
+    return ACDC_E_ALIGN;
+  const size_t need = acdc_bwd_workspace_bytes(rows, n);
+  if (ws_bytes < need) return ACDC_E_WS;
+  int logn;
+  int rc = check_n(n, &logn);
+  if (rc) return rc;
+  const LaunchInfo li = tm2_launch_info(logn);
+  int64_t grid;
+  if ((rc = grid_for(li, (rows + 1) / 2, &grid))) return rc;
+  Tables tb;
+  if ((rc = get_tables(logn, &tb))) return rc;
+  KParams p{};
+  p.x = x_hi;
+  p.dy = dy;
+  p.y = dx;
+  p.a = a_hi;
+  p.d = d_hi;
+  p.h2c = const_cast<float*>(h2_hi);
+  p.dy_gather = dy_gather_hi;
+  p.epi_relu = relu_hi;
+  p.ws = (float*)ws_hi;
+  p.x2 = x_lo;
+  p.a2 = a_lo;
+  p.d2 = d_lo;
+  p.h2c2 = h2_lo;
+  p.dy_gather2 = dy_gather_lo;
+  p.epi_relu2 = relu_lo;
+  p.ws2 = (float*)ws_lo;
+  p.tab = tb.tab;
+  p.rows = rows;
+  p.ldx = ldx_hi;
+  p.ldx2 = ldx_lo;
+  p.ldy = ldy;
+  p.ldo = lddx;
+#ifdef ACDC_NO_STAGE
+  p.stage = 0;
+#else
+  p.stage = (((uintptr_t)dy & 15) == 0 && (ldy & 3) == 0) ? 1 : 0;
+#endif
+  return launch(li, grid, &p, (cudaStream_t)stream);
 }
 
 int cascade_grad_reduce_f32(const void* ws, size_t ws_stride_bytes, int32_t blocks, int64_t rows, int32_t n,

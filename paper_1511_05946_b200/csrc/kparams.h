@@ -22,6 +22,15 @@ struct KParams {
   int stage;            // bwd (TMEM kernel): dy rows are 16-byte aligned -> bulk-copy them into smem ahead
   const int* dy_gather;  // bwd (TMEM kernel, fused cascade): dy[:, i] = dy_in[:, dy_gather[i]] (inverse perm)
   const float2* tab;  // [pass twiddles | c'_k]
+  // two-block cascade backward (acdc_bwd_tm2_kernel): the second (lower) block's operands
+  const float* x2;
+  const float* a2;
+  const float* d2;
+  const float* h2c2;
+  const int* dy_gather2;
+  float* ws2;
+  int epi_relu2;
+  int64_t ldx2;
   int64_t rows;
   int64_t ldx, ldy, ldo;
 };

@@ -14,6 +14,8 @@ from __future__ import annotations
 
 import ctypes
 
+import os
+
 import torch
 
 from . import _lib
@@ -582,9 +584,29 @@ def _cascade_backward_deferred(x, g, a, d, perm, fl, xs, h2, grads, tab, accumul
     lib = _lib.load()
     if any(t.shape != (n,) for gr in grads for t in gr):
         raise ValueError("gradient buffers must be contiguous fp32 (n,) tensors on the input device")
+    has_perm = any(f & 2 for f in fl[:-1])
+    pairs = (os.environ.get("ACDC_CASCADE_PAIR", "1") != "0" and depth >= 2 and (perm_inv is not None or not has_perm)
+             and lib.cascade_pair_supported(rows, n) == 1)
     with torch.cuda.device(dev):
         ws = torch.empty(depth * stride // 4, dtype=torch.float32, device=dev)
-        for l in range(depth - 1, -1, -1):
+        l = depth - 1
+        while pairs and l >= 1:  # blocks l (hi) and l-1 (lo) in one launch, the dx between them on chip
+            hi, lo = l, l - 1
+            xh = xs[hi - 1]
+            xlo = x if lo == 0 else xs[lo - 1]
+            gh = perm_inv[hi] if (perm_inv is not None and hi < depth - 1 and fl[hi] & 2) else None
+            gl = perm_inv[lo] if (perm_inv is not None and fl[lo] & 2) else None
+            out = torch.empty_like(g)
+            ah, dh = _vec(a[hi], n, dev, "a"), _vec(d[hi], n, dev, "d")
+            al, dl = _vec(a[lo], n, dev, "a"), _vec(d[lo], n, dev, "d")
+            _lib.check(lib.cascade_bwd_pair_defer_f32(
+                _ptr(xh), _ptr(xlo), _ptr(g), _ptr(out), _ptr(ah), _ptr(dh), _ptr(al), _ptr(dl), _ptr(h2[hi]),
+                _ptr(h2[lo]), _ptr(gh), _ptr(gl), 1 if fl[lo] & 1 else 0, 1 if (lo > 0 and fl[lo - 1] & 1) else 0,
+                ws.data_ptr() + hi * stride, ws.data_ptr() + lo * stride, stride, rows, n, _ld(xh, n),
+                _ld(xlo, n), _ld(g, n), n, _stream(x)))
+            g = out
+            l -= 2
+        for l in range(l, -1, -1):
             xl = x if l == 0 else xs[l - 1]
             prev = fl[l - 1] if l > 0 else 0
             if perm_inv is not None:  # the permutation after block l as this block's dy gather

@@ -182,3 +182,42 @@ def test_deferred_reduction_abi_errors():
     assert lib.cascade_defer_ws_bytes(0, 1024) == 0
     assert lib.cascade_grad_reduce_f32(None, 0, 0, 0, 1024, None, 0, None) == 0  # nothing to reduce
     assert lib.cascade_grad_reduce_f32(None, 1 << 20, 2, 64, 1000, None, 0, None) != 0  # not a power of two
+
+
+@pytest.mark.parametrize("n,depth,rows,relu,perm", [(512, 2, 6, True, True), (1024, 12, 130, True, True),
+                                                    (1024, 5, 33, True, True), (2048, 3, 64, False, True),
+                                                    (2048, 4, 40, True, False), (1024, 3, 17, False, False)])
+def test_two_block_backward_matches_one_block(n, depth, rows, relu, perm, monkeypatch):
+    """The two-block launch (block l+1's dx kept on chip as block l's dy) is
+    bit-identical to one launch per block, for even and odd depths, with and
+    without ReLU / permutations, odd row counts included."""
+    from paper_1511_05946_b200 import _lib
+
+    assert _lib.load().cascade_pair_supported(rows, n) == 1
+    rng = np.random.default_rng(11)
+    casc, layers, _ = build(n, depth, rng, relu=relu, perm=perm)
+    x = torch.as_tensor(f32(rng, rows, n), device=DEV)
+    dy = torch.as_tensor(f32(rng, rows, n), device=DEV)
+    acdc = [L for L in layers if hasattr(L, "grad_a")]
+    res = []
+    for pair in ("1", "0"):
+        monkeypatch.setenv("ACDC_CASCADE_PAIR", pair)
+        casc.zero_grads()
+        casc.forward(x)
+        dx = casc.backward(dy)
+        torch.cuda.synchronize()
+        res.append([dx.clone()] + [g.clone() for L in acdc for g in (L.grad_a, L.grad_d, L.grad_bias_d)])
+    for a_, b_ in zip(*res):
+        assert torch.equal(a_, b_)
+
+
+def test_two_block_abi_guards():
+    from paper_1511_05946_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.cascade_pair_supported(64, 256) == 0  # below the TMEM backward's sizes
+    assert lib.cascade_pair_supported(64, 16384) == 0
+    assert lib.cascade_pair_supported(0, 1024) == 0
+    assert lib.cascade_pair_supported(64, 4096) == 0  # the two blocks' stashes do not fit
+    assert lib.cascade_bwd_pair_defer_f32(*([None] * 12), 0, 0, None, None, 0, 64, 256, 256, 256, 256, 256,
+                                          None) != 0
