@@ -1547,6 +1547,11 @@ __global__ void __launch_bounds__(256) acdc_grad_final_kernel(const double* __re
 // (programmatic dependent launch; the kernel waits before reading).
 template <class... KA, class... A>
 static void launch_pdl(void (*kern)(KA...), dim3 grid, cudaStream_t st, A... args) {
+  static const bool co_set = [&] {
+    if (carveout_pref() >= 0) cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carveout_pref());
+    return true;
+  }();
+  (void)co_set;
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -3,6 +3,7 @@
 #include "runtime.h"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <map>
 #include <mutex>
@@ -129,6 +130,21 @@ static int build_tables(int logn, bool hl, Tables* out) {
 int get_tables(int logn, Tables* out) { return build_tables(logn, false, out); }
 int get_tables_hl(int logn, Tables* out) { return build_tables(logn, true, out); }
 
+// Preferred shared-memory carveout for every kernel, in percent (ACDC_CARVEOUT
+// overrides; -1: driver default).  50%: kernels that need more still get it
+// (N = 4096's 196 KB), the smaller ones keep a large L1 instead of the
+// driver's shared-memory-heavy choice.  Measured fwd+bwd at B = 16384
+// (profiles/round2/probes/carveout_ab.txt): N = 512 / 1024 / 2048 / 8192
+// -6% / -6% / -4% / -4%, N = 4096, C3, C4, C5 unchanged; 0% (smallest) costs
+// C4 +4% (the reduction kernels lose occupancy).
+int carveout_pref() {
+  static const int v = [] {
+    const char* e = std::getenv("ACDC_CARVEOUT");
+    return e ? std::atoi(e) : 50;
+  }();
+  return v;
+}
+
 int grid_for(const LaunchInfo& li, int64_t units, int64_t* grid) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -143,6 +159,8 @@ int grid_for(const LaunchInfo& li, int64_t units, int64_t* grid) {
         e = cudaFuncSetAttribute(li.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, li.smem);
         if (e != cudaSuccess) return set_cuda_error(e);
       }
+      if (const int co = carveout_pref(); co >= 0)
+        cudaFuncSetAttribute(li.fn, cudaFuncAttributePreferredSharedMemoryCarveout, co);
       int bps = 0, sms = 0;
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, li.fn, li.cta, li.smem);
       if (e != cudaSuccess) return set_cuda_error(e);

@@ -45,6 +45,8 @@ struct LaunchInfo {
 // Persistent grid: min(CTAs needed for `units` row groups, resident CTAs).
 // Sets the dynamic-smem attribute on first use.
 int grid_for(const LaunchInfo& li, int64_t units, int64_t* grid);
+// Preferred shared-memory carveout percent for every kernel (ACDC_CARVEOUT; -1: driver default).
+int carveout_pref();
 
 // Half-length plan (hl_kernels.cu): launch description for (logn, kind) if
 // that size / kind runs on it; hl_enabled(logn): the size runs on it.
