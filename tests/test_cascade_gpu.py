@@ -185,6 +185,7 @@ def test_deferred_reduction_abi_errors():
 
 
 @pytest.mark.parametrize("n,depth,rows,relu,perm", [(512, 2, 6, True, True), (1024, 12, 130, True, True),
+                                                    (1024, 4, 1, True, True), (512, 3, 2, True, True),
                                                     (1024, 5, 33, True, True), (2048, 3, 64, False, True),
                                                     (2048, 4, 40, True, False), (1024, 3, 17, False, False)])
 def test_two_block_backward_matches_one_block(n, depth, rows, relu, perm, monkeypatch):
