@@ -381,13 +381,19 @@ def run_ours(args):
     out = None
     if rank == 0:
         hbm, src = peaks()
-        # dominant kernel = the longer of fwd / bwd (bwd: backward kernel + grad reduce); the
-        # h2-cache backward is the TMEM kernel for 512 <= n <= 8192 (acdc_kernels.cu bwd_tm_ok)
+        # dominant kernel = the longer of fwd / bwd (bwd: backward kernel + grad reduce).  Which
+        # kernels run: the half-length plan for 2048 <= n <= 32768 (hl_kernels.cu ACDC_HL_MIN_LOGN,
+        # off with ACDC_HL=0), else the row-pair kernels, whose h2-cache backward is the TMEM kernel
+        # for 512 <= n (acdc_kernels.cu bwd_tm_ok)
+        hl = 2048 <= n <= 32768 and os.environ.get("ACDC_HL", "1") != "0"
         if bwd_ms >= fwd_ms:
-            bk = "acdc_bwd_tm_kernel" if (best["mode"] == "h2cache" and 512 <= n <= 8192) else "acdc_bwd_kernel"
+            if hl:
+                bk = "acdc_bwd_hl_kernel"
+            else:
+                bk = "acdc_bwd_tm_kernel" if (best["mode"] == "h2cache" and 512 <= n) else "acdc_bwd_kernel"
             kname, kms, kalg, kmov = f"{bk}(+grad_reduce)", bwd_ms, alg_bwd * B, mov_bwd * B
         else:
-            kname, kms, kalg, kmov = "acdc_fwd_kernel", fwd_ms, alg_fwd * B, mov_fwd * B
+            kname, kms, kalg, kmov = ("acdc_fwd_hl_kernel" if hl else "acdc_fwd_kernel"), fwd_ms, alg_fwd * B, mov_fwd * B
         achieved = kalg / (kms / 1e3) / 1e9
         step_alg = (alg_fwd + alg_bwd) * B
         step_gbs = step_alg / (ms_per_step / 1e3) / 1e9

@@ -200,9 +200,14 @@ __device__ __forceinline__ void hl_out(const float2 (&h)[16], float4 (&o)[8], co
 #ifndef ACDC_HL_FWD_CTA  // forward CTA size where a group is 256 threads (N = 8192): 3 groups, 85 registers
 #define ACDC_HL_FWD_CTA 768
 #endif
+#ifndef ACDC_HL_FWD_CTA128  // forward CTA size where a group is 128 threads (N = 4096)
+#define ACDC_HL_FWD_CTA128 512
+#endif
 template <int LOGN>
 constexpr int hl_fwd_gpc() {
-  return (Geo<LOGN - 1>::T == 256 && ACDC_HL_FWD_CTA == 768) ? 3 : 0;
+  return (Geo<LOGN - 1>::T == 256 && ACDC_HL_FWD_CTA == 768)   ? 3
+         : (Geo<LOGN - 1>::T == 128 && ACDC_HL_FWD_CTA128 > 512) ? ACDC_HL_FWD_CTA128 / 128
+                                                                  : 0;
 }
 template <int LOGN>
 using GeoHLF = GeoHL<LOGN, hl_fwd_gpc<LOGN>()>;
@@ -548,7 +553,7 @@ __global__ void ACDC_LB(GeoHL<LOGN>) acdc_bwd_hl_kernel(KParams p) {
 
 // ------------------------------------------------------------------ host
 #ifndef ACDC_HL_MIN_LOGN  // smallest size run on the half-length plan (the row-pair kernels below it)
-#define ACDC_HL_MIN_LOGN 13
+#define ACDC_HL_MIN_LOGN 11  // A/B fwd+bwd (h2 cache): N=2048 -8.4%, 4096 -4.6%; N=1024 +-0 stays row-pair
 #endif
 
 template <class K>
@@ -595,6 +600,15 @@ bool hl_launch_info(int logn, int kind, LaunchInfo* li) {
   if (!on || logn < ACDC_HL_MIN_LOGN || logn > 15) return false;
   if (kind != 0 && kind != 1 && kind != 4 && kind != 5) return false;
   switch (logn) {
+#if ACDC_HL_MIN_LOGN <= 12
+    case 12: hl_info<12>(kind, li); break;
+#endif
+#if ACDC_HL_MIN_LOGN <= 11
+    case 11: hl_info<11>(kind, li); break;
+#endif
+#if ACDC_HL_MIN_LOGN <= 10
+    case 10: hl_info<10>(kind, li); break;
+#endif
     case 13: hl_info<13>(kind, li); break;
     case 14: hl_info<14>(kind, li); break;
     case 15: hl_info<15>(kind, li); break;
