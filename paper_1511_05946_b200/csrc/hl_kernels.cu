@@ -205,9 +205,9 @@ __device__ __forceinline__ void hl_out(const float2 (&h)[16], float4 (&o)[8], co
 #endif
 template <int LOGN>
 constexpr int hl_fwd_gpc() {
-  return (Geo<LOGN - 1>::T == 256 && ACDC_HL_FWD_CTA == 768)   ? 3
-         : (Geo<LOGN - 1>::T == 128 && ACDC_HL_FWD_CTA128 > 512) ? ACDC_HL_FWD_CTA128 / 128
-                                                                  : 0;
+  return (Geo<LOGN - 1>::T == 256 && ACDC_HL_FWD_CTA == 768)    ? 3
+         : (Geo<LOGN - 1>::T == 128 && ACDC_HL_FWD_CTA128 != 512) ? ACDC_HL_FWD_CTA128 / 128
+                                                                   : 0;
 }
 template <int LOGN>
 using GeoHLF = GeoHL<LOGN, hl_fwd_gpc<LOGN>()>;
@@ -292,13 +292,22 @@ __global__ void ACDC_LB(GeoHLF<LOGN>) acdc_fwd_hl_kernel(KParams p) {
 }
 
 // ----------------------------------------------------------------- backward
+#ifndef ACDC_HL_BWD_CTA128  // backward CTA size where a group is 128 threads (N = 4096); 0: 512
+#define ACDC_HL_BWD_CTA128 0
+#endif
+template <int LOGN>
+constexpr int hl_bwd_gpc() {
+  return (Geo<LOGN - 1>::T == 128 && ACDC_HL_BWD_CTA128 > 0) ? ACDC_HL_BWD_CTA128 / 128 : 0;
+}
+template <int LOGN>
+using GeoHLB = GeoHL<LOGN, hl_bwd_gpc<LOGN>()>;
 template <int LOGN>
 __host__ __device__ constexpr bool hl_tm_a() {  // grad_a also in TMEM (else: the CTA's partial row in global memory)
-  return (GeoHL<LOGN>::CTA / 128) * 96 <= 512;
+  return (GeoHLB<LOGN>::CTA / 128) * 96 <= 512;
 }
 template <int LOGN>
 __host__ __device__ constexpr bool hl_tm_d() {  // d of the 32 slot bins also in TMEM (cols 96..127)
-  return (GeoHL<LOGN>::CTA / 128) * 128 <= 512;
+  return (GeoHLB<LOGN>::CTA / 128) * 128 <= 512;
 }
 template <int LOGN>
 __host__ __device__ constexpr int hl_ncol() {
@@ -306,7 +315,7 @@ __host__ __device__ constexpr int hl_ncol() {
 }
 template <int LOGN>
 __host__ __device__ constexpr int hl_cols() {
-  constexpr int need = (GeoHL<LOGN>::CTA / 128) * hl_ncol<LOGN>();
+  constexpr int need = (GeoHLB<LOGN>::CTA / 128) * hl_ncol<LOGN>();
   return need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
 }
 
@@ -325,8 +334,8 @@ __device__ __forceinline__ void tmem_st16f(uint32_t a, const float (&r)[16]) {
 
 // RECOMP: h2 = C2(a x) is recomputed instead of read from the cache.
 template <int LOGN, bool RECOMP>
-__global__ void ACDC_LB(GeoHL<LOGN>) acdc_bwd_hl_kernel(KParams p) {
-  using G = GeoHL<LOGN>;
+__global__ void ACDC_LB(GeoHLB<LOGN>) acdc_bwd_hl_kernel(KParams p) {
+  using G = GeoHLB<LOGN>;
   constexpr int T = G::T;
   constexpr int S = FastMap<G>::S;
   constexpr bool TMA = hl_tm_a<LOGN>();
@@ -573,7 +582,7 @@ static void hl_info(int kind, LaunchInfo* li) {
     li->max_per_sm = 512 / hl_fwd_cols<LOGN>();
     return;
   }
-  using G = GeoHL<LOGN>;
+  using G = GeoHLB<LOGN>;
   geom_hl<G>(*li);
   switch (kind) {
     case 1:
