@@ -15,8 +15,16 @@ namespace acdc {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // Whole warp: allocate COLS columns (power of two >= 32), base address -> *slot.
+// The CTA first initialises a (never used) mbarrier: compute-sanitizer's
+// synccheck (CUDA 12.9) reports "Barrier error. Missing init" at shared address
+// 0x0 and kills the kernel for a TMEM allocation in a CTA that has initialised
+// no mbarrier (scripts/synccheck_tmem_probe.cu: alloc + ld/st + dealloc alone
+// trips it, the same with one mbarrier.init first is clean).
 template <int COLS>
 __device__ __forceinline__ void tmem_alloc(uint32_t* slot) {
+  __shared__ __align__(8) uint64_t synccheck_bar;
+  if ((threadIdx.x & 31) == 0)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&synccheck_bar)) : "memory");
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "n"(COLS)
                : "memory");
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");

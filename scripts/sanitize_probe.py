@@ -6,7 +6,8 @@ of dy into the reused exchange buffer, TMEM alloc/dealloc, cross-group
 parking) launched back to back under PDL, the recompute backward, the
 two-stage gradient reduction (many row groups at N=128), the SGD-fused
 reduction followed by a dependent backward, the fused cascade forward and
-its block backwards (ReLU / inverse-perm epilogues, PDL chain), AFDF forward
+its block backwards (ReLU / inverse-perm epilogues, PDL chain; two-block
+launches and the deferred multi-block reduction), AFDF forward
 and backward, the complex FFT and the DCT / IDCT kernels.
 usage: python scripts/sanitize_probe.py
 """
@@ -43,6 +44,7 @@ layer(128, 2100, False)   # two-stage reduction (many row groups)
 layer(16384, 3, True)     # half-length plan (N/2-point FFT per row), TMEM accumulators
 layer(32768, 2, True)     # half-length plan, tables in global memory, grad_a partial in global memory
 layer(8192, 5, False)     # half-length recompute backward
+layer(2048, 9, True)      # half-length plan at its smallest size (the metric path's kernels, N/2 = 1024)
 # SGD-fused reduction, then a backward of the same layer (PDL ordering)
 n, rows = 1024, 10
 x, dy = rn(rows, n), rn(rows, n)
@@ -63,7 +65,14 @@ for i in range(3):
         ls += [ReluLayer(512, device=dev), PermutationLayer(512, perm=rng.permutation(512), device=dev)]
 c = Cascade(ls)
 c.forward(rn(9, 512))
-c.backward(rn(9, 512))
+c.backward(rn(9, 512))  # two-block backward (block pairs 2+1), block 0 alone, one multi-block reduction
+c.forward(rn(9, 512))
+c.backward(rn(9, 512), on_layer=lambda layer: None)  # per-block gather backward + reduction (hook path)
+# 4-block stack at N=1024 without permutations: two two-block launches, deferred reduction
+ls = [AcdcLayer(1024, device=dev) for _ in range(4)]
+c = Cascade(ls)
+c.forward(rn(7, 1024))
+c.backward(rn(7, 1024))
 # AFDF, FFT, DCT
 for n in (256, 8192):
     z = torch.complex(rn(5, n), rn(5, n))
