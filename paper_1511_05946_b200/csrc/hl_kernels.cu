@@ -310,6 +310,16 @@ __host__ __device__ constexpr bool hl_tm_d() {  // d of the 32 slot bins also in
   return (GeoHLB<LOGN>::CTA / 128) * 128 <= 512;
 }
 template <int LOGN>
+__host__ __device__ constexpr bool hl_cta_red() {  // one gradient partial per CTA (all accumulators in TMEM)
+#ifdef ACDC_HL_NO_CTA_RED
+  return GeoHLB<LOGN>::GPC == 1;
+#else
+  // group 0's thread t reads group g's thread t at the same TMEM lane: every group must span all
+  // four lane quadrants (T a multiple of 128)
+  return (hl_tm_a<LOGN>() && GeoHLB<LOGN>::T % 128 == 0) || GeoHLB<LOGN>::GPC == 1;
+#endif
+}
+template <int LOGN>
 __host__ __device__ constexpr int hl_ncol() {
   return hl_tm_d<LOGN>() ? 128 : (hl_tm_a<LOGN>() ? 96 : 64);
 }
@@ -529,11 +539,43 @@ __global__ void ACDC_LB(GeoHLB<LOGN>) acdc_bwd_hl_kernel(KParams p) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) po[q * S] = f4mul(__ldg(pa + q * S), g1[q]);
   }
-  // this group's partials: grad_d / grad_bias at the slot bins, grad_a at 4m..4m+3
+  // One partial per CTA where every accumulator is in TMEM: group 0's thread t
+  // reads the other groups' columns at its own lane (same lane quadrant) and
+  // adds them in group order, so the reduction sees one partial per CTA
+  // (single stage) instead of one per group.
+  constexpr bool CRED = hl_cta_red<LOGN>() && !RECOMP;  // (recompute: +11% from the extra registers, not used)
+  if constexpr (CRED && G::GPC > 1) {
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (c.grp != 0) {  // groups 1..: done (their columns are read by group 0)
+      tmem_fence_before();
+      __syncthreads();
+      tmem_fence_after();
+      if (warp == 0) tmem_dealloc<COLS>(tm_slot);
+      return;
+    }
+    wsg = p.ws + (int64_t)blockIdx.x * 3 * G::NR;
+    gag = reinterpret_cast<float4*>(wsg) + fm.jsp;
+  }
+  auto ld_sum16 = [&](uint32_t col, float (&acc)[16]) {  // this group's 16 columns (+ the others' in order)
+    tmem_ld16f(ta + col, acc);
+    if constexpr (CRED && G::GPC > 1) {
+#pragma unroll
+      for (int g = 1; g < G::GPC; ++g) {
+        float o[16];
+        // group g's thread t: warp + g T/32 (same lane quadrant), its column base
+        tmem_ld16f(tmem_addr(tm_slot, warp, ((warp + g * (T / 32)) >> 2) * NCOL) + col, o);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] += o[i];
+      }
+    }
+  };
+  // this group's (CTA's) partials: grad_d / grad_bias at the slot bins, grad_a at 4m..4m+3
 #pragma unroll
   for (int sp = 0; sp < 4; ++sp) {
     float acc[16];
-    tmem_ld16f(ta + 16 * sp, acc);
+    ld_sum16(16 * sp, acc);
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const HlSlot<G> sl(fm, 2 * sp + j);
@@ -548,7 +590,7 @@ __global__ void ACDC_LB(GeoHLB<LOGN>) acdc_bwd_hl_kernel(KParams p) {
 #pragma unroll
     for (int qp = 0; qp < 2; ++qp) {
       float acc[16];
-      tmem_ld16f(ta + 64 + 16 * qp, acc);
+      ld_sum16(64 + 16 * qp, acc);
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         gag[(4 * qp + j) * S] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
@@ -592,6 +634,7 @@ static void hl_info(int kind, LaunchInfo* li) {
       li->pdl = true;
 #endif
       li->max_per_sm = 512 / hl_cols<LOGN>();
+      if (hl_cta_red<LOGN>() && kind == 5) li->red_per_cta = 1;  // one partial per CTA (cached backward)
       break;
     default: li->fn = nullptr;
   }

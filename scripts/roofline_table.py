@@ -25,7 +25,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PROBES = {
     "m_cache": (4096, 16384, False), "m_recompute": (4096, 16384, False), "n128": (128, 16384, False),
     "n8192": (8192, 16384, False), "n16384": (16384, 16384, False), "n32768": (32768, 4096, False),
-    "c3": (1024, 8192, False), "c5": (8192, 8192, True),
+    "c3": (1024, 8192, False), "c5": (8192, 8192, True), "n1024": (1024, 16384, False),
+    "n2048": (2048, 16384, False), "n256": (256, 16384, False),
 }
 
 
@@ -43,6 +44,8 @@ def alg_bytes(kname, n, rows, cplx):
         return None
     if "cascade_fwd" in kname:
         return 2 * e * n * rows
+    if "bwd_tm2" in kname:  # two block backwards per launch
+        return 2 * 3 * e * n * rows
     if "fwd" in kname:
         return 2 * e * n * rows
     if "bwd" in kname:
