@@ -42,6 +42,12 @@
 #include "tma.cuh"
 #include "tmem.cuh"
 
+#ifndef ACDC_HL_H2_STREAM  // 1: the forward stores the h2 cache evict-first
+#define ACDC_HL_H2_STREAM 1
+#endif
+#ifndef ACDC_HL_Y_STREAM  // 1: the forward stores y evict-first
+#define ACDC_HL_Y_STREAM 0
+#endif
 #ifndef ACDC_HL_SLOT_DYN
 #define ACDC_HL_SLOT_DYN 0
 #endif
@@ -267,7 +273,14 @@ __global__ void ACDC_LB(GeoHLF<LOGN>) acdc_fwd_hl_kernel(KParams p) {
         hl_coefs<G>(cp, wn, fm, s, cA, cB, W);
         const HlSlot<G> sl(fm, s);
         float4 X = hl_post(v[s], w[s], cA, cB, W, sl.sp);
-        if constexpr (H2C) __stcs(reinterpret_cast<float4*>(p.h2c + r * G::NR) + s * T + t, X);
+        if constexpr (H2C) {
+          float4* hp = reinterpret_cast<float4*>(p.h2c + r * G::NR) + s * T + t;
+#if ACDC_HL_H2_STREAM
+          __stcs(hp, X);
+#else
+          *hp = X;  // normal caching: the last rows' h2 stays in L2 for the last-first backward
+#endif
+        }
         float db[8];
         tmem_ld8(ta + 8 * s, db);
         X.x = fmaf(X.x, db[0], db[4]);
@@ -283,7 +296,13 @@ __global__ void ACDC_LB(GeoHLF<LOGN>) acdc_fwd_hl_kernel(KParams p) {
     hl_out<G>(v, o, fm);
     float4* py = reinterpret_cast<float4*>(p.y + r * p.ldo) + fm.jsp;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) py[q * FastMap<G>::S] = o[q];
+    for (int q = 0; q < 8; ++q) {
+#if ACDC_HL_Y_STREAM
+      __stcs(py + q * FastMap<G>::S, o[q]);
+#else
+      py[q * FastMap<G>::S] = o[q];
+#endif
+    }
   }
   tmem_fence_before();
   __syncthreads();
