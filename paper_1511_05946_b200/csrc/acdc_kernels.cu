@@ -1411,6 +1411,8 @@ __device__ __forceinline__ bool reduce_cols(const float* __restrict__ ws, int64_
     const int64_t gstride = 3LL * n;
     int64_t g = s;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    // unrolled: the loads of several iterations are in flight together (the sums keep their order)
+#pragma unroll 4
     for (; g + 24 < groups; g += 32) {
       a0 += (double)base[g * gstride];
       a1 += (double)base[(g + 8) * gstride];
@@ -1505,6 +1507,7 @@ __global__ void __launch_bounds__(256) acdc_grad_partial_kernel(const float* __r
   const int64_t g1 = g0 + RED_CHUNK < groups ? g0 + RED_CHUNK : groups;
   double acc = 0.0;
   if (idx < total)
+#pragma unroll 10  // up to RED_CHUNK / 8 = 20 loads per thread, issued ahead of the (ordered) adds
     for (int64_t g = g0 + s; g < g1; g += 8) acc += (double)ws[g * total + idx];
   part[s][o] = acc;
   __syncthreads();
@@ -1526,6 +1529,7 @@ __global__ void __launch_bounds__(256) acdc_grad_final_kernel(const double* __re
   const int comp = (int)(idx / n);
   const int i = (int)(idx - (int64_t)comp * n);
   double t = 0.0;
+#pragma unroll 8
   for (int c = 0; c < chunks; ++c) t += tmp[(int64_t)c * total + idx];
   float* out = comp == 0 ? ga : (comp == 1 ? gd : gb);
   if (accumulate) t += (double)out[i];

@@ -505,6 +505,7 @@ __global__ void __launch_bounds__(256) afdf_grad_reduce_kernel(const float* __re
     const float* base = ws + comp * len + i;
     double a0 = 0.0, a1 = 0.0;
     int64_t g = s;
+#pragma unroll 4
     for (; g + 8 < groups; g += 16) {
       a0 += (double)base[g * total];
       a1 += (double)base[(g + 8) * total];
