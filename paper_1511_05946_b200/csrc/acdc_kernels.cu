@@ -1497,6 +1497,8 @@ __global__ void __launch_bounds__(256) acdc_grad_reduce_multi_kernel(const float
 // same epilogue as acdc_grad_reduce_kernel.  Deterministic for a fixed group
 // count.
 constexpr int RED_CHUNK = 160;
+// Up to this many partials the single-stage reduction (one kernel) is used.
+constexpr int RED_SINGLE_MAX = 320;
 __global__ void __launch_bounds__(256) acdc_grad_partial_kernel(const float* __restrict__ ws, int64_t groups,
                                                                 int64_t total, double* __restrict__ tmp) {
   pdl_wait();  // the backward's partials
@@ -1574,7 +1576,7 @@ static void launch_pdl(void (*kern)(KA...), dim3 grid, cudaStream_t st, A... arg
 
 // fp64 chunk-partial bytes the two-stage reduction needs after the partials.
 static size_t red_tmp_bytes(int64_t groups, int32_t n) {
-  if (groups <= RED_CHUNK) return 0;
+  if (groups <= RED_SINGLE_MAX) return 0;
   return (size_t)((groups + RED_CHUNK - 1) / RED_CHUNK) * 3 * (size_t)n * sizeof(double) + 8;
 }
 
@@ -1898,7 +1900,7 @@ int acdc_bwd_launch_count(int64_t rows, int32_t n, int cached) {
   LaunchInfo li;
   int64_t grid;
   if (sized(logn, cached ? K_BWD_H2 : K_BWD, rows, &li, &grid, true)) return -1;  // contiguous rows
-  return grid * (li.red_per_cta ? li.red_per_cta : li.gpc) > RED_CHUNK ? 3 : 2;  // backward + one or two reduction kernels
+  return grid * (li.red_per_cta ? li.red_per_cta : li.gpc) > RED_SINGLE_MAX ? 3 : 2;  // backward + one or two reductions
 }
 
 static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const float* a, const float* d,
@@ -1962,7 +1964,7 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
     if ((rc = plan_hl(logn, kind, p, &allow))) return rc;
     if ((rc = sized(logn, kind, rows, &li, &grid, allow))) return rc;
     groups = grid * (li.red_per_cta ? li.red_per_cta : li.gpc);
-    if (defer && groups > RED_CHUNK) return set_error(ACDC_E_SIZE, "deferred reduction: too many row groups");
+    if (defer && groups > RED_SINGLE_MAX) return set_error(ACDC_E_SIZE, "deferred reduction: too many row groups");
     scratch_floats = li.scratch;
     p.scratch = p.ws + groups * 3 * (int64_t)n;  // scratch follows the partials
     if ((rc = run(kind, p, n, st))) return rc;
@@ -1973,7 +1975,7 @@ static int bwd_impl(int kind, const float* x, const float* dy, float* dx, const 
   }
   const int64_t total = 3LL * n;
   int blocks = (int)((total + 31) / 32);
-  if (groups > RED_CHUNK) {
+  if (groups > RED_SINGLE_MAX) {
     const int chunks = (int)((groups + RED_CHUNK - 1) / RED_CHUNK);
     size_t off = (size_t)groups * (3 * (size_t)n + (size_t)scratch_floats) * sizeof(float);
     off = (off + 7) & ~(size_t)7;
@@ -2056,7 +2058,7 @@ static int64_t defer_groups(int64_t rows, int32_t n) {
   int64_t grid;
   if (sized(logn, K_BWD_H2_RP, rows, &li, &grid, true)) return 0;
   const int64_t groups = grid * (li.red_per_cta ? li.red_per_cta : li.gpc);
-  return groups <= RED_CHUNK ? groups : 0;
+  return groups <= RED_SINGLE_MAX ? groups : 0;
 }
 
 size_t cascade_defer_ws_bytes(int64_t rows, int32_t n) {

@@ -333,10 +333,15 @@ __host__ __device__ constexpr bool hl_cta_red() {  // one gradient partial per C
 #ifdef ACDC_HL_NO_CTA_RED
   return GeoHLB<LOGN>::GPC == 1;
 #else
-  // group 0's thread t reads group g's thread t at the same TMEM lane: every group must span all
-  // four lane quadrants (T a multiple of 128)
-  return (hl_tm_a<LOGN>() && GeoHLB<LOGN>::T % 128 == 0) || GeoHLB<LOGN>::GPC == 1;
+  // leader groups read their followers' columns at the same TMEM lanes (T a multiple or a divisor of 128)
+  return (hl_tm_a<LOGN>() && (GeoHLB<LOGN>::T % 128 == 0 || 128 % GeoHLB<LOGN>::T == 0)) ||
+         GeoHLB<LOGN>::GPC == 1;
 #endif
+}
+template <int LOGN>
+__host__ __device__ constexpr int hl_red_leaders() {  // partials per CTA with hl_cta_red
+  constexpr int L = GeoHLB<LOGN>::T >= 128 ? 1 : 128 / GeoHLB<LOGN>::T;
+  return L < GeoHLB<LOGN>::GPC ? L : GeoHLB<LOGN>::GPC;
 }
 template <int LOGN>
 __host__ __device__ constexpr int hl_ncol() {
@@ -558,33 +563,35 @@ __global__ void ACDC_LB(GeoHLB<LOGN>) acdc_bwd_hl_kernel(KParams p) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) po[q * S] = f4mul(__ldg(pa + q * S), g1[q]);
   }
-  // One partial per CTA where every accumulator is in TMEM: group 0's thread t
-  // reads the other groups' columns at its own lane (same lane quadrant) and
-  // adds them in group order, so the reduction sees one partial per CTA
-  // (single stage) instead of one per group.
+  // Fewer partials where every accumulator is in TMEM: a "leader" group l < L
+  // (L = max(1, 128 / T) groups cover the four TMEM lane quadrants) reads the
+  // columns of groups l + L, l + 2L, ... at its own lanes (thread t of group
+  // l + kL is warp + kLT/32: same quadrant) and adds them in group order, so the
+  // reduction sees L partials per CTA (single stage) instead of one per group.
   constexpr bool CRED = hl_cta_red<LOGN>() && !RECOMP;  // (recompute: +11% from the extra registers, not used)
-  if constexpr (CRED && G::GPC > 1) {
+  constexpr int L = hl_red_leaders<LOGN>();
+  if constexpr (CRED && G::GPC > L) {
     tmem_fence_before();
     __syncthreads();
     tmem_fence_after();
-    if (c.grp != 0) {  // groups 1..: done (their columns are read by group 0)
+    if (c.grp >= L) {  // non-leaders: done (their columns are read by the leaders)
       tmem_fence_before();
       __syncthreads();
       tmem_fence_after();
       if (warp == 0) tmem_dealloc<COLS>(tm_slot);
       return;
     }
-    wsg = p.ws + (int64_t)blockIdx.x * 3 * G::NR;
+    wsg = p.ws + ((int64_t)blockIdx.x * L + c.grp) * 3 * G::NR;
     gag = reinterpret_cast<float4*>(wsg) + fm.jsp;
   }
-  auto ld_sum16 = [&](uint32_t col, float (&acc)[16]) {  // this group's 16 columns (+ the others' in order)
+  auto ld_sum16 = [&](uint32_t col, float (&acc)[16]) {  // this group's 16 columns (+ its followers' in order)
     tmem_ld16f(ta + col, acc);
-    if constexpr (CRED && G::GPC > 1) {
+    if constexpr (CRED && G::GPC > L) {
 #pragma unroll
-      for (int g = 1; g < G::GPC; ++g) {
+      for (int k = 1; k < G::GPC / L; ++k) {
         float o[16];
-        // group g's thread t: warp + g T/32 (same lane quadrant), its column base
-        tmem_ld16f(tmem_addr(tm_slot, warp, ((warp + g * (T / 32)) >> 2) * NCOL) + col, o);
+        // group l + kL's thread t: warp + k L T / 32 (a multiple of 4: same lane quadrant)
+        tmem_ld16f(tmem_addr(tm_slot, warp, ((warp + k * L * (T / 32)) >> 2) * NCOL) + col, o);
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc[i] += o[i];
       }
@@ -653,7 +660,7 @@ static void hl_info(int kind, LaunchInfo* li) {
       li->pdl = true;
 #endif
       li->max_per_sm = 512 / hl_cols<LOGN>();
-      if (hl_cta_red<LOGN>() && kind == 5) li->red_per_cta = 1;  // one partial per CTA (cached backward)
+      if (hl_cta_red<LOGN>() && kind == 5) li->red_per_cta = hl_red_leaders<LOGN>();  // (cached backward)
       break;
     default: li->fn = nullptr;
   }
