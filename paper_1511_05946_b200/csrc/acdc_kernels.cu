@@ -118,6 +118,9 @@ __device__ __forceinline__ void packed_dct3(float2 (&Y)[G::E], float2 (&v)[G::E]
 #ifndef ACDC_BWD_CTA
 #define ACDC_BWD_CTA 0
 #endif
+#ifndef ACDC_FWD_PDL  // forward kernels launched with programmatic dependent launch
+#define ACDC_FWD_PDL 1
+#endif
 #ifndef ACDC_PF_DIST  // L2 prefetch distance in row-pair iterations (fast-pairing kernels)
 #define ACDC_PF_DIST 1
 #endif
@@ -161,7 +164,13 @@ __global__ void ACDC_LB(GeoFwd<LOGN>) acdc_fwd_kernel(KParams p) {
   Xbuf<G> xb{smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS, 0};
   constexpr bool PST = fwd_pstash_bytes<LOGN>() > 0;
   float4* pst = reinterpret_cast<float4*>(smem_f + G::SMEM_BYTES / 4) + t;
-  if constexpr (PST && G::FP) {  // group 0 fills; stage_tables' barrier publishes it
+  const float2 *tw, *cp;
+  stage_tables<G>(p.tab, smem_f, tw, cp);  // (constant tables: may overlap the previous kernel)
+  // launched with programmatic dependent launch: everything below reads / writes
+  // what the previous kernels of the stream may still use (a / d / bias after a
+  // fused SGD step, the h2 cache a previous backward reads, x / y)
+  pdl_wait();
+  if constexpr (PST && G::FP) {  // group 0 fills, the barrier below publishes it
     const FastMap<G> fm(t, gs.mask);
     if (c.grp == 0) {
 #pragma unroll
@@ -169,9 +178,8 @@ __global__ void ACDC_LB(GeoFwd<LOGN>) acdc_fwd_kernel(KParams p) {
         pst[s * G::T] = make_float4(__ldg(fm.plo(p.d, s)), __ldg(fm.phi(p.d, s)), __ldg(fm.plo(p.bias, s)),
                                     __ldg(fm.phi(p.bias, s)));
     }
+    __syncthreads();
   }
-  const float2 *tw, *cp;
-  stage_tables<G>(p.tab, smem_f, tw, cp);
   const int64_t npairs = (p.rows + 1) >> 1;
   if constexpr (G::FP) {
     const FastMap<G> fm(t, gs.mask);
@@ -1607,6 +1615,9 @@ static LaunchInfo info_for(int kind) {
       li.fn = (const void*)acdc_fwd_kernel<LOGN, false>;
       geom<GF>(li, 0);
       li.smem += fwd_pstash_bytes<LOGN>();
+#ifndef ACDC_NO_PDL
+      li.pdl = ACDC_FWD_PDL;  // table staging overlaps the previous kernel (pdl_wait before any data access)
+#endif
       break;
     case K_BWD:
       li.fn = (const void*)acdc_bwd_kernel<LOGN, false>;
@@ -1629,6 +1640,9 @@ static LaunchInfo info_for(int kind) {
       li.fn = FP ? (const void*)acdc_fwd_kernel<LOGN, FP> : nullptr;
       geom<GF>(li, 0);
       li.smem += fwd_pstash_bytes<LOGN>();
+#ifndef ACDC_NO_PDL
+      li.pdl = ACDC_FWD_PDL;
+#endif
       break;
     default:
 #ifndef ACDC_NO_BWD_TM

@@ -251,6 +251,9 @@ __global__ void ACDC_LB(GeoHLF<LOGN>) acdc_fwd_hl_kernel(KParams p) {
   if constexpr (!G::TW_SMEM) __syncthreads();
   tmem_fence_after();
   const uint32_t ta = tmem_addr(tm_slot, warp, (warp >> 2) * 64);
+  // programmatic dependent launch: the prologue above (constant tables, TMEM)
+  // may overlap the previous kernel; d / bias, x, y and the h2 cache only after
+  pdl_wait();
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
     const HlSlot<G> sl(fm, s);
@@ -648,6 +651,9 @@ static void hl_info(int kind, LaunchInfo* li) {
     geom_hl<GeoHLF<LOGN>>(*li);
     li->fn = kind == 0 ? (const void*)acdc_fwd_hl_kernel<LOGN, false> : (const void*)acdc_fwd_hl_kernel<LOGN, true>;
     li->max_per_sm = 512 / hl_fwd_cols<LOGN>();
+#if !defined(ACDC_NO_PDL) && (!defined(ACDC_FWD_PDL) || ACDC_FWD_PDL)
+    li->pdl = true;  // the prologue overlaps the previous kernel (pdl_wait before any data access)
+#endif
     return;
   }
   using G = GeoHLB<LOGN>;
