@@ -577,16 +577,12 @@ __global__ void ACDC_LB(GeoHLB<LOGN>) acdc_bwd_hl_kernel(KParams p) {
     tmem_fence_before();
     __syncthreads();
     tmem_fence_after();
-    if (c.grp >= L) {  // non-leaders: done (their columns are read by the leaders)
-      tmem_fence_before();
-      __syncthreads();
-      tmem_fence_after();
-      if (warp == 0) tmem_dealloc<COLS>(tm_slot);
-      return;
-    }
+    // non-leaders skip the writes (their columns are read by the leaders) and meet
+    // everyone at the final barrier (one barrier site for the whole CTA)
     wsg = p.ws + ((int64_t)blockIdx.x * L + c.grp) * 3 * G::NR;
     gag = reinterpret_cast<float4*>(wsg) + fm.jsp;
   }
+  const bool writer = !(CRED && G::GPC > L) || c.grp < L;
   auto ld_sum16 = [&](uint32_t col, float (&acc)[16]) {  // this group's 16 columns (+ its followers' in order)
     tmem_ld16f(ta + col, acc);
     if constexpr (CRED && G::GPC > L) {
@@ -601,6 +597,7 @@ __global__ void ACDC_LB(GeoHLB<LOGN>) acdc_bwd_hl_kernel(KParams p) {
     }
   };
   // this group's (CTA's) partials: grad_d / grad_bias at the slot bins, grad_a at 4m..4m+3
+  if (writer) {
 #pragma unroll
   for (int sp = 0; sp < 4; ++sp) {
     float acc[16];
@@ -625,6 +622,7 @@ __global__ void ACDC_LB(GeoHLB<LOGN>) acdc_bwd_hl_kernel(KParams p) {
         gag[(4 * qp + j) * S] = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
     }
   }
+  }  // writer
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
