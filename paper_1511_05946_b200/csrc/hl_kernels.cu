@@ -42,6 +42,12 @@
 #include "tma.cuh"
 #include "tmem.cuh"
 
+#ifndef ACDC_HL_FWD_LD16  // 1: the forward loads the d / bias of two slots per TMEM load
+#define ACDC_HL_FWD_LD16 0
+#endif
+#ifndef ACDC_HL_BWD_LD1  // 1: the backward loads its accumulators and d with one completion wait
+#define ACDC_HL_BWD_LD1 0
+#endif
 #ifndef ACDC_HL_H2_STREAM  // 1: the forward stores the h2 cache evict-first
 #define ACDC_HL_H2_STREAM 1
 #endif
@@ -202,6 +208,19 @@ __device__ __forceinline__ void hl_out(const float2 (&h)[16], float4 (&o)[8], co
   }
 }
 
+__device__ __forceinline__ void tmem_ld16f(uint32_t a, float (&r)[16]) {
+  float2 v[8];
+  tmem_ld16(a, v);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r[2 * i] = v[i].x, r[2 * i + 1] = v[i].y;
+}
+__device__ __forceinline__ void tmem_st16f(uint32_t a, const float (&r)[16]) {
+  float2 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = make_float2(r[2 * i], r[2 * i + 1]);
+  tmem_st16(a, v);
+}
+
 // ------------------------------------------------------------------ forward
 #ifndef ACDC_HL_FWD_CTA  // forward CTA size where a group is 256 threads (N = 8192): 3 groups, 85 registers
 #define ACDC_HL_FWD_CTA 768
@@ -270,8 +289,14 @@ __global__ void ACDC_LB(GeoHLF<LOGN>) acdc_fwd_hl_kernel(KParams p) {
     {
       float2 w[8], gl[8], gh[8];
       fp_partner<G>(v, w, fm);
+#if ACDC_HL_FWD_LD16
+      float db16[16];  // d / bias of slots 2k, 2k+1: one TMEM load (one completion wait) per slot pair
+#endif
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
+#if ACDC_HL_FWD_LD16
+        if ((s & 1) == 0) tmem_ld16f(ta + 8 * s, db16);
+#endif
         float2 cA, cB, W;
         hl_coefs<G>(cp, wn, fm, s, cA, cB, W);
         const HlSlot<G> sl(fm, s);
@@ -285,7 +310,12 @@ __global__ void ACDC_LB(GeoHLF<LOGN>) acdc_fwd_hl_kernel(KParams p) {
 #endif
         }
         float db[8];
+#if ACDC_HL_FWD_LD16
+#pragma unroll
+        for (int i = 0; i < 8; ++i) db[i] = db16[8 * (s & 1) + i];
+#else
         tmem_ld8(ta + 8 * s, db);
+#endif
         X.x = fmaf(X.x, db[0], db[4]);
         X.y = fmaf(X.y, db[1], db[5]);
         X.z = fmaf(X.z, db[2], db[6]);
@@ -354,19 +384,6 @@ template <int LOGN>
 __host__ __device__ constexpr int hl_cols() {
   constexpr int need = (GeoHLB<LOGN>::CTA / 128) * hl_ncol<LOGN>();
   return need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
-}
-
-__device__ __forceinline__ void tmem_ld16f(uint32_t a, float (&r)[16]) {
-  float2 v[8];
-  tmem_ld16(a, v);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) r[2 * i] = v[i].x, r[2 * i + 1] = v[i].y;
-}
-__device__ __forceinline__ void tmem_st16f(uint32_t a, const float (&r)[16]) {
-  float2 v[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = make_float2(r[2 * i], r[2 * i + 1]);
-  tmem_st16(a, v);
 }
 
 // RECOMP: h2 = C2(a x) is recomputed instead of read from the cache.
@@ -495,8 +512,13 @@ __global__ void ACDC_LB(GeoHLB<LOGN>) acdc_bwd_hl_kernel(KParams p) {
 #pragma unroll
       for (int sp = 0; sp < 4; ++sp) {
         float acc[16], dd[8];
+#if ACDC_HL_BWD_LD1
+        if constexpr (hl_tm_d<LOGN>()) tmem_ld16_ld8(ta + 16 * sp, acc, ta + 96 + 8 * sp, dd);  // one wait
+        else tmem_ld16f(ta + 16 * sp, acc);
+#else
         tmem_ld16f(ta + 16 * sp, acc);
         if constexpr (hl_tm_d<LOGN>()) tmem_ld8(ta + 96 + 8 * sp, dd);
+#endif
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int s = 2 * sp + j;

@@ -75,6 +75,26 @@ __device__ __forceinline__ void tmem_ld16(uint32_t a, float2 (&v)[8]) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = make_float2(__uint_as_float(u[2 * i]), __uint_as_float(u[2 * i + 1]));
 }
+// 16 columns at a16 and 8 at a8 with ONE completion wait (two loads in flight).
+__device__ __forceinline__ void tmem_ld16_ld8(uint32_t a16, float (&r16)[16], uint32_t a8, float (&r8)[8]) {
+  uint32_t u[16], w[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7]),
+        "=r"(u[8]), "=r"(u[9]), "=r"(u[10]), "=r"(u[11]), "=r"(u[12]), "=r"(u[13]), "=r"(u[14]), "=r"(u[15])
+      : "r"(a16)
+      : "memory");
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+               : "r"(a8)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) r16[i] = __uint_as_float(u[i]);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r8[i] = __uint_as_float(w[i]);
+}
 __device__ __forceinline__ void tmem_st16(uint32_t a, const float2 (&v)[8]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "

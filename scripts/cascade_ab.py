@@ -40,11 +40,26 @@ def timeit(fn, steps=10):
     return e0.elapsed_time(e1) / steps
 
 
+def graphed(step):
+    step()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        step()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            step()
+    torch.cuda.synchronize()
+    return g.replay
+
+
 def main():
     dev = torch.device("cuda", 0)
     rng = np.random.default_rng(0)
     for n, depth, rows, rp in ((4096, 32, 4096, False), (4096, 12, 4096, True), (2048, 12, 8192, True),
-                               (1024, 12, 8192, True)):
+                               (2048, 32, 8192, False), (1024, 12, 8192, True)):
         casc = stack(n, depth, rp, dev, rng)
         x = torch.randn(rows, n, device=dev)
         dy = torch.randn(rows, n, device=dev)
@@ -55,11 +70,14 @@ def main():
 
         fused = casc._fused
         ms_f = timeit(step)
+        ms_fg = timeit(graphed(step))
         casc._fused = None
         ms_u = timeit(step)
+        ms_ug = timeit(graphed(step))
         casc._fused = fused
         print(json.dumps({"n": n, "depth": depth, "rows": rows, "relu_perm": rp, "fused_ms": ms_f,
-                          "per_layer_ms": ms_u, "per_layer_over_fused": ms_u / ms_f}), flush=True)
+                          "per_layer_ms": ms_u, "fused_graph_ms": ms_fg, "per_layer_graph_ms": ms_ug,
+                          "per_layer_over_fused_graph": ms_ug / ms_fg}), flush=True)
         del casc
         torch.cuda.empty_cache()
 
