@@ -185,14 +185,16 @@ def c3(args, dev):
         casc.forward(x)
         casc.backward(dy)
 
-    ms_f = timeit(step, args.steps)
+    ms_f_eager = timeit(step, args.steps)
+    ms_f = timeit(graphed(step), args.steps)  # the same step replayed from a CUDA graph
     fused = casc._fused
     casc._fused = None
     ms_u = timeit(step, max(3, args.steps // 4))
     casc._fused = fused
     # bytes: x, y, dy, dx (16N) + checkpoints x_l (K-1) and h2_l (K) written once, read once
     bytes_row = 16 * n + 2 * 4 * n * ((depth - 1) + depth)
-    return {"config": "C3 12-block ACDC+ReLU+Perm cascade N=1024 batch 8192", "fused_ms": ms_f, "unfused_ms": ms_u,
+    return {"config": "C3 12-block ACDC+ReLU+Perm cascade N=1024 batch 8192 (CUDA-graph replay)", "fused_ms": ms_f,
+            "fused_ms_eager": ms_f_eager, "unfused_ms": ms_u,
             "fused_rows_per_s": B / (ms_f / 1e3), "unfused_rows_per_s": B / (ms_u / 1e3),
             "fused_speedup": ms_u / ms_f, "fused_bytes_per_row": bytes_row,
             "fused_hbm_frac": B / (ms_f / 1e3) * bytes_row / (peak_hbm() * 1e9)}
@@ -300,8 +302,13 @@ def c5(args, dev):
         dp.allreduce_grads()
 
     ms = timeit_dist(step, args.steps)
+    if world == 1:  # replay of the captured step (eager above: the multi-rank path)
+        ms_eager = ms
+        ms = timeit(graphed(step), args.steps)
     rps = total / (ms / 1e3)
     return {"config": f"C5 AFDF N=8192 complex64, {total} rows over {world} GPU(s)", "n_gpus": world,
+            "timing": "CUDA-graph replay" if world == 1 else "eager",
+            **({"ms_per_step_eager": ms_eager} if world == 1 else {}),
             "rows_per_gpu": B, "ms_per_step": ms, "rows_per_s": rps, "rows_per_s_per_gpu": rps / world,
             "bytes_per_row": 40 * n, "hbm_roofline_frac_per_gpu": rps / world * 40 * n / (peak_hbm() * 1e9),
             "scaling": "strong"}
