@@ -407,10 +407,10 @@ def run_ours(args):
     if rank == 0:
         hbm, src = peaks()
         # dominant kernel = the longer of fwd / bwd (bwd: backward kernel + grad reduce).  Which
-        # kernels run: the half-length plan for 2048 <= n <= 32768 (hl_kernels.cu ACDC_HL_MIN_LOGN,
+        # kernels run: the half-length plan for 1024 <= n <= 32768 (hl_kernels.cu ACDC_HL_MIN_LOGN,
         # off with ACDC_HL=0), else the row-pair kernels, whose h2-cache backward is the TMEM kernel
         # for 512 <= n (acdc_kernels.cu bwd_tm_ok)
-        hl = 2048 <= n <= 32768 and os.environ.get("ACDC_HL", "1") != "0"
+        hl = 1024 <= n <= 32768 and os.environ.get("ACDC_HL", "1") != "0"
         if bwd_ms >= fwd_ms:
             if hl:
                 bk = "acdc_bwd_hl_kernel"

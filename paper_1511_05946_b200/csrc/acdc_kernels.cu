@@ -1506,7 +1506,10 @@ __global__ void __launch_bounds__(256) acdc_grad_reduce_multi_kernel(const float
 // count.
 constexpr int RED_CHUNK = 160;
 // Up to this many partials the single-stage reduction (one kernel) is used.
-constexpr int RED_SINGLE_MAX = 320;
+#ifndef ACDC_RED_SINGLE_MAX
+#define ACDC_RED_SINGLE_MAX 640  // A/B at N=1024 (592 partials): single stage -1.2% step against two stages
+#endif
+constexpr int RED_SINGLE_MAX = ACDC_RED_SINGLE_MAX;
 __global__ void __launch_bounds__(256) acdc_grad_partial_kernel(const float* __restrict__ ws, int64_t groups,
                                                                 int64_t total, double* __restrict__ tmp) {
   pdl_wait();  // the backward's partials

@@ -653,7 +653,7 @@ __global__ void ACDC_LB(GeoHLB<LOGN>) acdc_bwd_hl_kernel(KParams p) {
 
 // ------------------------------------------------------------------ host
 #ifndef ACDC_HL_MIN_LOGN  // smallest size run on the half-length plan (the row-pair kernels below it)
-#define ACDC_HL_MIN_LOGN 11  // A/B fwd+bwd (h2 cache): N=2048 -8.4%, 4096 -4.6%; N=1024 +-0 stays row-pair
+#define ACDC_HL_MIN_LOGN 10  // A/B fwd+bwd (h2 cache): N=1024 -4.4%, 2048 -8.4%, 4096 -4.6%
 #endif
 
 template <class K>

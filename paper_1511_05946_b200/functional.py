@@ -64,8 +64,8 @@ def _rows2d(x: torch.Tensor, n: int, name: str = "x") -> torch.Tensor:
         x = x.float()
     if x.stride(1) != 1 or (x.shape[0] > 1 and x.stride(0) < n):
         x = x.contiguous()
-    elif n >= 8192 and x.numel() and (x.data_ptr() % 16 or (x.shape[0] > 1 and x.stride(0) % 4)):
-        x = x.contiguous()  # the half-length large-N kernels move rows as 128-bit quads
+    elif n >= 1024 and x.numel() and (x.data_ptr() % 16 or (x.shape[0] > 1 and x.stride(0) % 4)):
+        x = x.contiguous()  # the half-length-plan kernels (n >= 1024) move rows as 128-bit quads
     return x
 
 
