@@ -92,7 +92,7 @@ int acdc_bwd_f32(const float* x, const float* dy, float* dx, const float* a, con
  * bytes, opaque layout); acdc_bwd_cached_f32 reads it instead of recomputing
  * C2(a*x), trading 8n bytes/row of HBM traffic for one of the backward's three
  * transforms.  Same results as the pair above.  256 <= n <= 32768 (bytes() == 0
- * otherwise).  For n >= 8192 the kernels run the half-length plan (one
+ * otherwise).  For n >= 1024 the kernels run the half-length plan (one
  * n/2-point complex FFT per row) and need 16-byte aligned rows with ld a
  * multiple of 4 (ACDC_E_ALIGN otherwise); the cache layout follows the plan,
  * so a cache is only valid for the backward of the same size. */
