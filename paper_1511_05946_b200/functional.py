@@ -13,7 +13,6 @@ Reference counterparts (under /root/reference/pkg/src/acdc):
 from __future__ import annotations
 
 import ctypes
-
 import os
 
 import torch
