@@ -1,4 +1,4 @@
-"""GPU tier: the half-length plan for long rows (hl_kernels.cu, N >= 8192:
+"""GPU tier: the half-length plan (hl_kernels.cu, N >= 1024:
 one N/2-point complex FFT per row) against the fp64 oracle, with and without
 the h2 cache, odd / single-row batches, the ACDC_HL=0 row-pair kernels as a
 second implementation, and alignment handling at the C ABI.
@@ -24,8 +24,8 @@ def f32(rng, *shape, mean=0.0, std=1.0):
     return (mean + std * rng.standard_normal(shape)).astype(np.float32)
 
 
-@pytest.mark.parametrize("n", [8192, 16384, 32768])
-@pytest.mark.parametrize("rows", [1, 4, 7])
+@pytest.mark.parametrize("n,rows", [(n, r) for n in (1024, 2048, 4096, 8192, 16384, 32768) for r in (1, 4, 7)]
+                         + [(1024, 601), (2048, 601), (4096, 601)])  # 601: many CTAs, leader reductions, idle groups
 @pytest.mark.parametrize("cached", [True, False])
 def test_hl_vs_oracle(n, rows, cached):
     from paper_1511_05946_b200 import functional as F
