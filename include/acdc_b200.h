@@ -234,6 +234,26 @@ int cascade_bwd_pair_defer_f32(const float* x_hi, const float* x_lo, const float
                                int32_t n, int64_t ldx_hi, int64_t ldx_lo, int64_t ldy, int64_t lddx,
                                acdc_stream_t stream);
 
+/* Fused cascade of ACDC-only blocks (the reference's acdc_cascade) on the
+ * half-length plan, 1024 <= n <= 16384 (cascade_hl_supported(n) != 0):
+ * cascade_fwd_hl_f32 runs every block on chip like cascade_fwd_f32 and writes
+ * the same checkpoint buffer (cascade_ckpt_bytes), with the h2 caches in this
+ * plan's layout; 16-byte aligned rows and parameters.  Block l's backward is
+ * the single-layer cached backward (acdc_bwd_cached_f32 with h2cache = block
+ * l's cache), or, deferred, cascade_bwd_hl_defer_f32 into a block-private
+ * workspace of cascade_hl_defer_ws_bytes bytes and one
+ * cascade_grad_reduce_hl_f32 for all blocks (arguments as
+ * cascade_grad_reduce_f32). */
+int cascade_hl_supported(int32_t n);
+int cascade_fwd_hl_f32(const float* x, float* y, int32_t depth, int32_t n, const float* a, const float* d,
+                       const float* bias, float* ckpt, int64_t rows, int64_t ldx, int64_t ldy, acdc_stream_t stream);
+size_t cascade_hl_defer_ws_bytes(int64_t rows, int32_t n);
+int cascade_bwd_hl_defer_f32(const float* x, const float* dy, float* dx, const float* a, const float* d,
+                             const float* h2cache, void* ws, size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx,
+                             int64_t ldy, int64_t lddx, acdc_stream_t stream);
+int cascade_grad_reduce_hl_f32(const void* ws, size_t ws_stride_bytes, int32_t blocks, int64_t rows, int32_t n,
+                               float* const* grads, int accumulate, acdc_stream_t stream);
+
 /* ---- ReLU and Permutation layers outside the fused cascade (layers.py:218-265) ----
  * acdc_relu_fwd_f32: y = x > 0 ? x : 0 (strict mask, layers.py:227).
  * acdc_relu_bwd_f32: dx = y > 0 ? dy : 0, with y the forward's OUTPUT

@@ -95,6 +95,12 @@ SIGNATURES = {
     ),
     "cascade_grad_reduce_f32": (ctypes.c_int, [_P, ctypes.c_size_t, _I32, _I64, _I32, _P, ctypes.c_int, _P]),
     "cascade_pair_supported": (ctypes.c_int, [_I64, _I32]),
+    "cascade_hl_supported": (ctypes.c_int, [_I32]),
+    "cascade_fwd_hl_f32": (ctypes.c_int, [_P, _P, _I32, _I32, _P, _P, _P, _P, _I64, _I64, _I64, _P]),
+    "cascade_hl_defer_ws_bytes": (ctypes.c_size_t, [_I64, _I32]),
+    "cascade_bwd_hl_defer_f32": (
+        ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, ctypes.c_size_t, _I64, _I32, _I64, _I64, _I64, _P]),
+    "cascade_grad_reduce_hl_f32": (ctypes.c_int, [_P, ctypes.c_size_t, _I32, _I64, _I32, _P, ctypes.c_int, _P]),
     "cascade_bwd_pair_defer_f32": (
         ctypes.c_int,
         [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int, ctypes.c_int, _P, _P, ctypes.c_size_t, _I64,

@@ -2068,12 +2068,13 @@ int cascade_bwd_block_gather_f32(const float* x, const float* dy, float* dx, con
 
 // Row groups of the block backward (its partials per workspace), or 0 where
 // the deferred reduction does not apply.
-static int64_t defer_groups(int64_t rows, int32_t n) {
+static int64_t defer_groups(int64_t rows, int32_t n, int kind = K_BWD_H2_RP) {
   int logn;
   if (rows <= 0 || check_n(n, &logn) || acdc_h2cache_bytes(rows, n) == 0) return 0;
+  if (kind == K_BWD_H2 && !hl_enabled(logn)) return 0;  // (the half-length cascade's blocks)
   LaunchInfo li;
   int64_t grid;
-  if (sized(logn, K_BWD_H2_RP, rows, &li, &grid, true)) return 0;
+  if (sized(logn, kind, rows, &li, &grid, true)) return 0;
   const int64_t groups = grid * (li.red_per_cta ? li.red_per_cta : li.gpc);
   return groups <= RED_SINGLE_MAX ? groups : 0;
 }
@@ -2096,6 +2097,37 @@ int cascade_bwd_block_defer_f32(const float* x, const float* dy, float* dx, cons
   if ((prev_perm || dy_gather) && dx == dy) return set_error(ACDC_E_SHAPE, "the permuted block backward cannot write in place");
   return bwd_impl(K_BWD_H2_RP, x, dy, dx, a, d, h2cache, nullptr, nullptr, nullptr, 0, ws, ws_bytes, rows, n, ldx,
                   ldy, lddx, stream, prev_perm, prev_relu, nullptr, dy_gather, true);
+}
+
+// Half-length fused cascade (cascade_fwd_hl_f32): block backwards are the
+// single-layer cached backward on that plan; deferred partials as above.
+size_t cascade_hl_defer_ws_bytes(int64_t rows, int32_t n) {
+  if (defer_groups(rows, n, K_BWD_H2) == 0) return 0;
+  const size_t b = acdc_bwd_workspace_bytes(rows, n);
+  return (b + 255) & ~(size_t)255;
+}
+
+int cascade_bwd_hl_defer_f32(const float* x, const float* dy, float* dx, const float* a, const float* d,
+                             const float* h2cache, void* ws, size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx,
+                             int64_t ldy, int64_t lddx, acdc_stream_t stream) {
+  if (rows > 0 && defer_groups(rows, n, K_BWD_H2) == 0)
+    return set_error(ACDC_E_SIZE, "deferred half-length backward: unsupported size (see cascade_hl_defer_ws_bytes)");
+  return bwd_impl(K_BWD_H2, x, dy, dx, a, d, h2cache, nullptr, nullptr, nullptr, 0, ws, ws_bytes, rows, n, ldx, ldy,
+                  lddx, stream, nullptr, 0, nullptr, nullptr, true);
+}
+
+int cascade_grad_reduce_hl_f32(const void* ws, size_t ws_stride_bytes, int32_t blocks, int64_t rows, int32_t n,
+                               float* const* grads, int accumulate, acdc_stream_t stream) {
+  if (blocks <= 0 || rows <= 0) return blocks < 0 || rows < 0 ? ACDC_E_SHAPE : ACDC_OK;
+  const int64_t groups = defer_groups(rows, n, K_BWD_H2);
+  if (groups == 0) return set_error(ACDC_E_SIZE, "deferred reduction: unsupported size (see cascade_hl_defer_ws_bytes)");
+  if (!ws || !grads) return ACDC_E_NULL;
+  if (ws_stride_bytes % sizeof(float) || ws_stride_bytes < acdc_bwd_workspace_bytes(rows, n)) return ACDC_E_WS;
+  const int blocks_x = (int)((3LL * n + 31) / 32);
+  launch_pdl(acdc_grad_reduce_multi_kernel, dim3(blocks_x, blocks), (cudaStream_t)stream, (const float*)ws,
+             (int64_t)(ws_stride_bytes / sizeof(float)), groups, n, grads, accumulate);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
 }
 
 int cascade_pair_supported(int64_t rows, int32_t n) {

@@ -212,7 +212,8 @@ size_t cascade_ckpt_bytes(int64_t rows, int32_t n, int32_t depth) {
   if (n < 256 || n > 16384 || (n & (n - 1)) != 0 || rows < 0 || depth < 1) return 0;
   const size_t xck = (size_t)(depth - 1) * (size_t)rows * n;
   const size_t h2 = (size_t)depth * (size_t)((rows + 1) / 2) * 2 * n;
-  return (xck + h2) * sizeof(float);
+  const size_t pst = (size_t)depth * 2 * n;  // the half-length cascade's parameter re-layout (cascade_fwd_hl_f32)
+  return (xck + h2 + pst) * sizeof(float);
 }
 
 int cascade_fwd_f32(const float* x, float* y, int32_t depth, int32_t n, const float* a, const float* d,

@@ -180,6 +180,25 @@ __device__ __forceinline__ void hl_pre(float4 Y, float2 cA, float2 cB, float2 W,
 __device__ __forceinline__ float4 ld_row_f4(const float4* p) { return __ldg(p); }
 __device__ __forceinline__ float4 f4mul(float4 a, float4 b) { return make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w); }
 
+// Pass-0 inputs from a row already in registers as the quads hl_out produces
+// (o[q] = x[4m..4m+3], m = jsp + q*S), scaled by a: the fused cascade feeds a
+// layer's output into the next layer without a round trip through memory.
+template <class G>
+__device__ __forceinline__ void hl_from_quads(float2 (&v)[16], const float4 (&o)[8], const float* sc,
+                                              const FastMap<G>& fm) {
+  constexpr int S = FastMap<G>::S;
+  const float4* ps = reinterpret_cast<const float4*>(sc) + fm.jsp;
+  float2 snd[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 f = f4mul(o[q], __ldg(ps + q * S));
+    v[q] = make_float2(f.x, f.z);
+    snd[q] = make_float2(f.w, f.y);
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[15 - q] = fm.xor_shfl(snd[q]);
+}
+
 // Pass-0 inputs of one row: z[m] = (x[4m], x[4m+2]) kept, (x[4m+3], x[4m+1]) sent to the partner's slot 15-q.
 template <class G, bool SCALE>
 __device__ __forceinline__ void hl_load(float2 (&v)[16], const float* x, const float* sc, const FastMap<G>& fm) {
@@ -341,6 +360,104 @@ __global__ void ACDC_LB(GeoHLF<LOGN>) acdc_fwd_hl_kernel(KParams p) {
   __syncthreads();
   tmem_fence_after();
   if (warp == 0) tmem_dealloc<COLS>(tm_slot);
+}
+
+// Fused cascade of ACDC-only blocks on the half-length plan (the reference's
+// acdc_cascade, layers.py:360-362, Cascade.forward 336-339): every row runs
+// through all `depth` layers on chip, each layer's output feeding the next
+// layer's first FFT in registers (hl_from_quads); checkpoints for the
+// backward: x_{l+1} (natural rows, [depth-1][rows][N]) and h2_l (this plan's
+// cache layout, [depth][rows][N]) so each block's backward is the single-layer
+// cached backward (acdc_bwd_hl_kernel).  d / bias of every layer are read per
+// slot from global memory (L1 / L2): too many layers to stage in TMEM.
+struct CHParams {
+  const float* x;
+  float* y;
+  const float* a;     // [depth][N]
+  const float* d;     // [depth][N]
+  const float* bias;  // [depth][N]
+  float* xck;         // [depth-1][rows][N]
+  float* h2c;         // [depth][h2_stride]: block l's rows at h2c + l * h2_stride + r * N
+  const float4* pstash;  // [depth][8 slots][2][T]: d / bias at each thread's slot bins (cascade_hl_pstash_kernel)
+  const float2* tab;
+  int64_t rows, ldx, ldy, h2_stride;
+  int depth;
+};
+
+// d / bias of every layer re-laid out per thread and slot, [layer][slot][2][t]
+// float4 ((d at the slot's four bins), (bias at them)): the cascade forward
+// then reads two coalesced 128-bit values per slot instead of eight scalars.
+template <int LOGN>
+__global__ void cascade_hl_pstash_kernel(const float* d, const float* bias, float4* out, int depth) {
+  using G = GeoHLF<LOGN>;
+  constexpr int T = G::T, N = G::NR;
+  const int t = threadIdx.x;  // one group's threads (T <= 1024)
+  const int l = blockIdx.x;
+  const FastMap<G> fm(t, 0xffffffffu);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const HlSlot<G> sl(fm, s);
+    const float* dl = d + (int64_t)l * N;
+    const float* bl = bias + (int64_t)l * N;
+    float4* o = out + ((int64_t)l * 8 + s) * 2 * T + t;
+    o[0] = make_float4(dl[sl.b[0]], dl[sl.b[1]], dl[sl.b[2]], dl[sl.b[3]]);
+    o[T] = make_float4(bl[sl.b[0]], bl[sl.b[1]], bl[sl.b[2]], bl[sl.b[3]]);
+  }
+}
+
+template <int LOGN>
+__global__ void ACDC_LB(GeoHLF<LOGN>) cascade_fwd_hl_kernel(CHParams p) {
+  using G = GeoHLF<LOGN>;
+  constexpr int T = G::T, N = G::NR;
+  pdl_launch_dependents();
+  extern __shared__ __align__(16) float smem_f[];
+  const auto c = group_ctx<G>();
+  const int t = c.t;
+  GroupSync<G> gs(c.grp);
+  Xbuf<G> xb{smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS, 0};
+  const FastMap<G> fm(t, gs.mask);
+  const float2 *tw, *cp, *wn;
+  stage_tables_hl<G>(p.tab, smem_f, tw, cp, wn);
+  if constexpr (!G::TW_SMEM) __syncthreads();
+  pdl_wait();
+  for (int64_t r = c.gid; r < p.rows; r += c.gstride) {
+    if (t == 0 && r + c.gstride < p.rows) prefetch_row_l2(p.x + (r + c.gstride) * p.ldx, N);
+    float2 v[16];
+    hl_load<G, true>(v, p.x + r * p.ldx, p.a, fm);
+#pragma unroll 1
+    for (int l = 0; l < p.depth; ++l) {
+      const float4* pst = p.pstash + (int64_t)l * 16 * T + t;  // [slot][2][t]
+      fft_passes<G, 0, true>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
+      {
+        float2 w[8], gl[8], gh[8];
+        fp_partner<G>(v, w, fm);
+        float4* hp = reinterpret_cast<float4*>(p.h2c + (int64_t)l * p.h2_stride + r * N) + t;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+          float2 cA, cB, W;
+          hl_coefs<G>(cp, wn, fm, s, cA, cB, W);
+          const HlSlot<G> sl(fm, s);
+          float4 X = hl_post(v[s], w[s], cA, cB, W, sl.sp);
+          __stcs(hp + s * T, X);
+          const float4 dv = __ldg(pst + 2 * s * T), bv = __ldg(pst + (2 * s + 1) * T);
+          X.x = fmaf(X.x, dv.x, bv.x);
+          X.y = fmaf(X.y, dv.y, bv.y);
+          X.z = fmaf(X.z, dv.z, bv.z);
+          X.w = fmaf(X.w, dv.w, bv.w);
+          hl_pre(X, cA, cB, W, sl.sp, gl[s], gh[s]);
+        }
+        fp_scatter<G>(gl, gh, v, fm);
+      }
+      fft_passes<G, 0, true>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
+      float4 o[8];
+      hl_out<G>(v, o, fm);
+      float4* po = reinterpret_cast<float4*>(l + 1 < p.depth ? p.xck + ((int64_t)l * p.rows + r) * N
+                                                             : p.y + r * p.ldy) + fm.jsp;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) po[q * FastMap<G>::S] = o[q];
+      if (l + 1 < p.depth) hl_from_quads<G>(v, o, p.a + (int64_t)(l + 1) * N, fm);
+    }
+  }
 }
 
 // ----------------------------------------------------------------- backward
@@ -721,9 +838,111 @@ bool hl_launch_info(int logn, int kind, LaunchInfo* li) {
   return li->fn != nullptr;
 }
 
+// Fused ACDC-only cascade on the half-length plan: launch description, or
+// fn == nullptr where the size is not on the plan.
+template <int LOGN>
+static void hl_cascade_info(LaunchInfo* li) {
+  geom_hl<GeoHLF<LOGN>>(*li);
+  li->fn = (const void*)cascade_fwd_hl_kernel<LOGN>;
+  li->scratch = GeoHLF<LOGN>::T;  // (threads of one group: the parameter re-layout kernel's block)
+}
+template <int LOGN>
+static void hl_cascade_pstash(const float* d, const float* bias, float4* out, int depth, cudaStream_t st) {
+  cascade_hl_pstash_kernel<LOGN><<<depth, GeoHLF<LOGN>::T, 0, st>>>(d, bias, out, depth);
+}
+static void hl_cascade_pstash_launch(int logn, const float* d, const float* bias, float4* out, int depth,
+                                     cudaStream_t st) {
+  switch (logn) {
+#if ACDC_HL_MIN_LOGN <= 10
+    case 10: hl_cascade_pstash<10>(d, bias, out, depth, st); break;
+#endif
+#if ACDC_HL_MIN_LOGN <= 11
+    case 11: hl_cascade_pstash<11>(d, bias, out, depth, st); break;
+#endif
+#if ACDC_HL_MIN_LOGN <= 12
+    case 12: hl_cascade_pstash<12>(d, bias, out, depth, st); break;
+#endif
+    case 13: hl_cascade_pstash<13>(d, bias, out, depth, st); break;
+    case 14: hl_cascade_pstash<14>(d, bias, out, depth, st); break;
+    default: break;
+  }
+}
+static bool hl_cascade_launch_info(int logn, LaunchInfo* li) {
+  LaunchInfo probe;
+  // N >= 4096: below it the row-pair cascade's two-block backward wins (A/B, 32 blocks at N = 2048:
+  // +7.7% on this plan; N = 4096: -4.2%)
+  if (logn < 12 || logn > 14 || !hl_launch_info(logn, 4, &probe)) return false;
+  switch (logn) {
+#if ACDC_HL_MIN_LOGN <= 10
+    case 10: hl_cascade_info<10>(li); return true;
+#endif
+#if ACDC_HL_MIN_LOGN <= 11
+    case 11: hl_cascade_info<11>(li); return true;
+#endif
+#if ACDC_HL_MIN_LOGN <= 12
+    case 12: hl_cascade_info<12>(li); return true;
+#endif
+    case 13: hl_cascade_info<13>(li); return true;
+    case 14: hl_cascade_info<14>(li); return true;
+    default: return false;
+  }
+}
+
 bool hl_enabled(int logn) {
   LaunchInfo li;
   return hl_launch_info(logn, 0, &li);
 }
 
 }  // namespace acdc
+
+using namespace acdc;
+
+extern "C" {
+
+int cascade_hl_supported(int32_t n) {
+  int logn;
+  if (check_n(n, &logn)) return 0;
+  LaunchInfo li;
+  return hl_cascade_launch_info(logn, &li) ? 1 : 0;
+}
+
+int cascade_fwd_hl_f32(const float* x, float* y, int32_t depth, int32_t n, const float* a, const float* d,
+                       const float* bias, float* ckpt, int64_t rows, int64_t ldx, int64_t ldy, acdc_stream_t stream) {
+  int logn;
+  int rc = check_n(n, &logn);
+  if (rc) return rc;
+  LaunchInfo li;
+  if (!hl_cascade_launch_info(logn, &li) || depth < 1)
+    return set_error(ACDC_E_SIZE, "the half-length fused cascade needs 1024 <= n <= 16384 and depth >= 1");
+  if (rows == 0) return ACDC_OK;
+  if (rows < 0 || ldx < n || ldy < n) return ACDC_E_SHAPE;
+  if (!x || !y || !a || !d || !bias || !ckpt) return ACDC_E_NULL;
+  const bool quads = (((uintptr_t)x | (uintptr_t)y | (uintptr_t)a | (uintptr_t)ckpt) & 15) == 0 &&
+                     (rows == 1 || ((ldx & 3) == 0 && (ldy & 3) == 0));
+  if (!quads) return set_error(ACDC_E_ALIGN, "the half-length fused cascade needs 16-byte aligned rows");
+  Tables tb;
+  if ((rc = get_tables_hl(logn, &tb))) return rc;
+  int64_t grid;
+  if ((rc = grid_for(li, rows, &grid))) return rc;
+  CHParams p{};
+  p.x = x;
+  p.y = y;
+  p.a = a;
+  p.d = d;
+  p.bias = bias;
+  p.xck = ckpt;
+  p.h2c = ckpt + (size_t)(depth - 1) * (size_t)rows * n;
+  p.h2_stride = ((rows + 1) / 2) * 2 * (int64_t)n;  // the cascade checkpoint layout (cascade_ckpt_bytes)
+  // parameter re-layout after the checkpoints (cascade_ckpt_bytes reserves depth x 2n floats there)
+  float4* pst = reinterpret_cast<float4*>(p.h2c + (size_t)depth * p.h2_stride);
+  hl_cascade_pstash_launch(logn, d, bias, pst, depth, (cudaStream_t)stream);
+  p.pstash = pst;
+  p.tab = tb.tab;
+  p.rows = rows;
+  p.ldx = ldx;
+  p.ldy = ldy;
+  p.depth = depth;
+  return launch(li, grid, &p, (cudaStream_t)stream);
+}
+
+}  // extern "C"

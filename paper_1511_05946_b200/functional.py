@@ -431,8 +431,13 @@ def cascade_supported(n: int) -> bool:
     return 256 <= n <= 16384 and (n & (n - 1)) == 0
 
 
+def cascade_hl_supported(n: int) -> bool:
+    """Sizes where ACDC-only stacks run the half-length-plan fused cascade."""
+    return cascade_supported(n) and _lib.load().cascade_hl_supported(int(n)) == 1
+
+
 def cascade_forward(x: torch.Tensor, a: torch.Tensor, d: torch.Tensor, bias: torch.Tensor, perm: torch.Tensor | None,
-                    flags: torch.Tensor, out=None):
+                    flags: torch.Tensor, out=None, hl: bool = False):
     """Fused forward of ``depth`` blocks  x <- perm(relu(ACDC(x)))  (layers.py:336-339).
 
     a, d, bias: (depth, n) fp32; perm: (depth, n) int32 or None; flags: (depth,)
@@ -451,8 +456,12 @@ def cascade_forward(x: torch.Tensor, a: torch.Tensor, d: torch.Tensor, bias: tor
     if x.shape[0] == 0:
         return y, ckpt
     with torch.cuda.device(dev):
-        _lib.check(lib.cascade_fwd_f32(_ptr(x), _ptr(y), depth, n, _ptr(a), _ptr(d), _ptr(bias), _ptr(perm),
-                                       _ptr(flags), _ptr(ckpt), x.shape[0], _ld(x, n), _ld(y, n), _stream(x)))
+        if hl:  # ACDC-only stack on the half-length plan (x, y, params 16-byte aligned: _rows2d / contiguous)
+            _lib.check(lib.cascade_fwd_hl_f32(_ptr(x), _ptr(y), depth, n, _ptr(a), _ptr(d), _ptr(bias), _ptr(ckpt),
+                                              x.shape[0], _ld(x, n), _ld(y, n), _stream(x)))
+        else:
+            _lib.check(lib.cascade_fwd_f32(_ptr(x), _ptr(y), depth, n, _ptr(a), _ptr(d), _ptr(bias), _ptr(perm),
+                                           _ptr(flags), _ptr(ckpt), x.shape[0], _ld(x, n), _ld(y, n), _stream(x)))
     return y, ckpt
 
 
@@ -466,7 +475,7 @@ def _ckpt_views(ckpt: torch.Tensor, rows: int, n: int, depth: int):
 
 def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor | None, flags,
                      ckpt: torch.Tensor, grads, accumulate: bool = True, sgd=None, on_block=None,
-                     perm_inv: torch.Tensor | None = None) -> torch.Tensor:
+                     perm_inv: torch.Tensor | None = None, hl: bool = False) -> torch.Tensor:
     """Backward of :func:`cascade_forward` (layers.py:341-344): one cached-h2
     block backward per block, last to first, each applying the previous block's
     ReLU mask and inverse permutation in its epilogue.  ``a``, ``d``: sequences
@@ -501,6 +510,8 @@ def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor
     xs, h2 = _ckpt_views(ckpt, rows, n, depth)
     fl = [int(f) for f in flags]
     lib = _lib.load()
+    if hl:  # checkpoints from cascade_fwd_hl_f32: every block is a plain single-layer cached backward
+        return _cascade_backward_hl(x, g, a, d, xs, h2, grads, accumulate, sgd, on_block)
     gather = sgd is None and perm_inv is not None and lib.cascade_gather_supported(n) == 1
     # Without a per-block hook or fused SGD, every block writes only its
     # gradient partials and one launch reduces all blocks at the end: the
@@ -548,6 +559,47 @@ def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor
                 _ptr(ga), _ptr(gd), _ptr(gb), 1 if accumulate else 0, _ptr(ws), wsb, rows, n, _ld(xl, n), _ld(g, n),
                 n, _stream(x)))
             g = out
+            if on_block is not None:
+                on_block(l)
+    return g
+
+
+def _cascade_backward_hl(x, g, a, d, xs, h2, grads, accumulate, sgd, on_block):
+    """Backward of the half-length-plan cascade (ACDC-only blocks): deferred
+    block partials + one multi-block reduction, or (per-block hook / fused
+    SGD) the single-layer cached backward per block."""
+    depth = len(a)
+    n = a[0].shape[0]
+    rows = x.shape[0]
+    dev = x.device
+    lib = _lib.load()
+    stride = lib.cascade_hl_defer_ws_bytes(rows, n) if (sgd is None and on_block is None) else 0
+    tab = _grad_table(grads, dev) if stride else None
+    with torch.cuda.device(dev):
+        if tab is not None:
+            if any(t.shape != (n,) for gr in grads for t in gr):
+                raise ValueError("gradient buffers must be contiguous fp32 (n,) tensors on the input device")
+            ws = torch.empty(depth * stride // 4, dtype=torch.float32, device=dev)
+            for l in range(depth - 1, -1, -1):
+                xl = x if l == 0 else xs[l - 1]
+                out = torch.empty_like(g)
+                al, dl = _vec(a[l], n, dev, "a"), _vec(d[l], n, dev, "d")
+                _lib.check(lib.cascade_bwd_hl_defer_f32(
+                    _ptr(xl), _ptr(g), _ptr(out), _ptr(al), _ptr(dl), _ptr(h2[l]), ws.data_ptr() + l * stride,
+                    stride, rows, n, _ld(xl, n), _ld(g, n), n, _stream(x)))
+                g = out
+            _lib.check(lib.cascade_grad_reduce_hl_f32(_ptr(ws), stride, depth, rows, n, _ptr(tab),
+                                                      1 if accumulate else 0, _stream(x)))
+            return g
+        for l in range(depth - 1, -1, -1):
+            xl = x if l == 0 else xs[l - 1]
+            if sgd is not None:
+                prm, vel, lr3, wd3, mu = sgd[l]
+                g = acdc_backward_sgd(xl, g, prm, vel, lr3, wd3, mu, grads=grads[l], accumulate=accumulate,
+                                      h2cache=h2[l])
+            else:
+                ga, gd, gb = grads[l]
+                g = acdc_backward(xl, g, a[l], d[l], ga, gd, gb, accumulate=accumulate, h2cache=h2[l])
             if on_block is not None:
                 on_block(l)
     return g

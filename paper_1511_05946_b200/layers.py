@@ -423,8 +423,11 @@ class Cascade:
             rows = [torch.as_tensor(b[2].perm if b[2] is not None else np.arange(n), dtype=torch.int32) for b in blocks]
             perm = torch.stack(rows).to(dev).contiguous()
             perm_inv = torch.argsort(perm.long(), dim=1).to(torch.int32).contiguous()
+        # ACDC-only stacks (the reference's acdc_cascade) at the half-length plan's sizes run its fused
+        # cascade (cascade_fwd_hl_f32 + the single-layer cached backward per block)
+        hl = not any(flags) and F.cascade_hl_supported(n)
         return {"blocks": blocks, "flags": flags, "flags_t": torch.tensor(flags, dtype=torch.uint8, device=dev),
-                "perm": perm, "perm_inv": perm_inv, "n": n, "device": dev}
+                "perm": perm, "perm_inv": perm_inv, "n": n, "device": dev, "hl": hl}
 
     @property
     def fused(self) -> bool:
@@ -448,7 +451,7 @@ class Cascade:
             a = torch.stack([l.a for l in acdc])
             d = torch.stack([l.d for l in acdc])
             bias = torch.stack([l.bias_d for l in acdc])
-            y, ckpt = F.cascade_forward(xt, a, d, bias, fz["perm"], fz["flags_t"])
+            y, ckpt = F.cascade_forward(xt, a, d, bias, fz["perm"], fz["flags_t"], hl=fz["hl"])
             self._cache = (xt, ckpt)
             return Layer._out(y, host)
         if host:
@@ -477,7 +480,7 @@ class Cascade:
             hook = (lambda l: on_layer(acdc[l])) if on_layer is not None else None
             dx = F.cascade_backward(xt, gy, [l.a for l in acdc], [l.d for l in acdc], fz["perm"], fz["flags"], ckpt,
                                     [(l.grad_a, l.grad_d, l.grad_bias_d) for l in acdc], accumulate=True, sgd=sgd,
-                                    on_block=hook, perm_inv=fz["perm_inv"])
+                                    on_block=hook, perm_inv=fz["perm_inv"], hl=fz["hl"])
             return Layer._out(dx, host)
         g = grad_y
         if host:

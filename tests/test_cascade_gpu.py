@@ -222,3 +222,44 @@ def test_two_block_abi_guards():
     assert lib.cascade_pair_supported(64, 4096) == 0  # the two blocks' stashes do not fit
     assert lib.cascade_bwd_pair_defer_f32(*([None] * 12), 0, 0, None, None, 0, 64, 256, 256, 256, 256, 256,
                                           None) != 0
+
+
+@pytest.mark.parametrize("n,depth,rows", [(4096, 3, 17), (4096, 12, 40), (4096, 2, 5), (4096, 1, 3), (8192, 3, 9),
+                                          (16384, 2, 4), (4096, 4, 601)])
+def test_hl_cascade_vs_oracle_and_paths(n, depth, rows):
+    """ACDC-only stacks (the reference's acdc_cascade) at the half-length plan's
+    sizes: the fused cascade (cascade_fwd_hl_f32 + deferred block backwards)
+    against the fp64 oracle, and bit-identical to the per-block reductions
+    (hook path) and to the per-layer (unfused) AcdcLayer path."""
+    from paper_1511_05946_b200 import functional as F
+
+    rng = np.random.default_rng(n + depth)
+    casc, layers, specs = build(n, depth, rng, relu=False, perm=False, std=0.1)
+    assert casc._fused is not None and casc._fused["hl"] and F.cascade_hl_supported(n)
+    x = f32(rng, rows, n)
+    dy = f32(rng, rows, n)
+    xt, dyt = torch.as_tensor(x, device=DEV), torch.as_tensor(dy, device=DEV)
+    acdc = [L for L in layers if hasattr(L, "grad_a")]
+    res = []
+    for mode in ("deferred", "hook", "unfused"):
+        casc.zero_grads()
+        fused = casc._fused
+        if mode == "unfused":
+            casc._fused = None
+        y = casc.forward(xt)
+        dx = casc.backward(dyt, on_layer=(lambda layer: None) if mode == "hook" else None)
+        casc._fused = fused
+        torch.cuda.synchronize()
+        res.append([y.clone(), dx.clone()] + [g.clone() for L in acdc for g in (L.grad_a, L.grad_d, L.grad_bias_d)])
+    for a_, b_, c_ in zip(*res):
+        assert torch.equal(a_, b_)
+        assert torch.equal(a_, c_)
+    yr, caches = O.cascade_forward(x.astype(np.float64), specs)
+    dxr, grads = O.cascade_backward(dy.astype(np.float64), specs, caches)
+    grads = [g for g in grads if g is not None]
+    gains = [1.0] * depth
+    close(res[0][0], yr, O.chain_factor(gains) * O.fp32_tolerance(n, yr) * 2, "y")
+    close(res[0][1], dxr, O.chain_factor(gains) * O.fp32_tolerance(n, dxr) * 2, "dx")
+    for l, L in enumerate(acdc):
+        for k, (mine, ref) in enumerate(zip((L.grad_a, L.grad_d, L.grad_bias_d), grads[l])):
+            close(mine, ref, depth * O.grad_tolerance(n, rows, ref) * 2, f"block {l} grad {k}")
