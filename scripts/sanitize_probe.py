@@ -73,6 +73,14 @@ ls = [AcdcLayer(1024, device=dev) for _ in range(4)]
 c = Cascade(ls)
 c.forward(rn(7, 1024))
 c.backward(rn(7, 1024))
+# ACDC-only stack at N=4096: half-length fused cascade (parameter re-layout, blocks chained in registers),
+# deferred half-length block backwards, then the per-block path (hook)
+ls = [AcdcLayer(4096, device=dev) for _ in range(3)]
+c = Cascade(ls)
+c.forward(rn(5, 4096))
+c.backward(rn(5, 4096))
+c.forward(rn(5, 4096))
+c.backward(rn(5, 4096), on_layer=lambda layer: None)
 # AFDF, FFT, DCT
 for n in (256, 8192):
     z = torch.complex(rn(5, n), rn(5, n))
