@@ -23,6 +23,23 @@
 #endif
 namespace acdc {
 
+// d / bias of every block re-laid out per thread and slot, [block][slot][t]
+// float4 (d_lo, d_hi, b_lo, b_hi): the forward reads one coalesced 128-bit
+// value per slot and block instead of four scalar loads.
+template <int LOGN>
+__global__ void cascade_pstash_kernel(const float* d, const float* bias, float4* out) {
+  using G = Geo<LOGN>;
+  constexpr int T = G::T, N = G::N;
+  const int t = threadIdx.x;  // one group's threads
+  const int l = blockIdx.x;
+  const FastMap<G> fm(t, 0xffffffffu);
+  const float* dl = d + (int64_t)l * N;
+  const float* bl = bias + (int64_t)l * N;
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+    out[((int64_t)l * 8 + s) * T + t] = make_float4(*fm.plo(dl, s), *fm.phi(dl, s), *fm.plo(bl, s), *fm.phi(bl, s));
+}
+
 struct CParams {
   const float* x;
   float* y;
@@ -33,6 +50,7 @@ struct CParams {
   const uint8_t* flags;  // [K]: bit0 ReLU after block l, bit1 permutation after it
   float* xck;            // [K-1][rows][N]: x_{l+1}
   float* h2c;            // [K][npairs][2N]: h2_l cache
+  const float4* pstash;  // [K][8 slots][T]: (d_lo, d_hi, b_lo, b_hi) per thread (cascade_pstash_kernel)
   const float2* tab;
   int64_t rows, ldx, ldy;
   int depth;
@@ -81,13 +99,10 @@ __global__ void ACDC_LB(Geo<LOGN>) cascade_fwd_kernel(CParams p) {
       for (int q = 0; q < 8; ++q) an[q] = ld_f2(pav + 2 * q * S);
     }
     for (int l = 0; l < p.depth; ++l) {
-      const float* dl = p.d + (int64_t)l * N;
-      const float* bl = p.bias + (int64_t)l * N;
       // d_l / bias_l of this thread's spectral slots: in flight across the first transform
       float4 dbv[8];
 #pragma unroll
-      for (int s = 0; s < 8; ++s)
-        dbv[s] = make_float4(__ldg(fm.plo(dl, s)), __ldg(fm.phi(dl, s)), __ldg(fm.plo(bl, s)), __ldg(fm.phi(bl, s)));
+      for (int s = 0; s < 8; ++s) dbv[s] = __ldg(p.pstash + ((int64_t)l * 8 + s) * T + t);
       float2 v[16];
       {
 #pragma unroll
@@ -184,6 +199,27 @@ static LaunchInfo cinfo() {
   return li;
 }
 
+template <int LOGN>
+static void pstash_launch(const float* d, const float* bias, float4* out, int depth, cudaStream_t st) {
+  cascade_pstash_kernel<LOGN><<<depth, Geo<LOGN>::T, 0, st>>>(d, bias, out);
+}
+static void pstash_for(int logn, const float* d, const float* bias, float4* out, int depth, cudaStream_t st) {
+  switch (logn) {
+#ifndef ACDC_ONLY_LOGN
+    case 8: pstash_launch<8>(d, bias, out, depth, st); break;
+    case 9: pstash_launch<9>(d, bias, out, depth, st); break;
+    case 10: pstash_launch<10>(d, bias, out, depth, st); break;
+    case 11: pstash_launch<11>(d, bias, out, depth, st); break;
+    case 12: pstash_launch<12>(d, bias, out, depth, st); break;
+    case 13: pstash_launch<13>(d, bias, out, depth, st); break;
+    case 14: pstash_launch<14>(d, bias, out, depth, st); break;
+#elif ACDC_ONLY_LOGN >= 8 && ACDC_ONLY_LOGN <= 14
+    case ACDC_ONLY_LOGN: pstash_launch<ACDC_ONLY_LOGN>(d, bias, out, depth, st); break;
+#endif
+    default: break;
+  }
+}
+
 static int cinfo_for(int logn, LaunchInfo* li) {
   switch (logn) {
 #ifndef ACDC_ONLY_LOGN
@@ -245,6 +281,10 @@ int cascade_fwd_f32(const float* x, float* y, int32_t depth, int32_t n, const fl
   p.xck = ckpt;
   p.h2c = ckpt + (size_t)(depth - 1) * (size_t)rows * n;
   p.tab = tb.tab;
+  // parameter re-layout after the checkpoints (cascade_ckpt_bytes reserves depth x 2n floats: 8 T float4 per block)
+  float4* pst = reinterpret_cast<float4*>(p.h2c + (size_t)depth * (size_t)((rows + 1) / 2) * 2 * n);
+  pstash_for(logn, d, bias, pst, depth, (cudaStream_t)stream);
+  p.pstash = pst;
   p.rows = rows;
   p.ldx = ldx;
   p.ldy = ldy;
