@@ -387,9 +387,14 @@ struct CHParams {
 // d / bias of every layer re-laid out per thread and slot, [layer][slot][2][t]
 // float4 ((d at the slot's four bins), (bias at them)): the cascade forward
 // then reads two coalesced 128-bit values per slot instead of eight scalars.
+// The cascade forward keeps two layers' worth of state live: 512-thread CTAs (128 registers) at
+// every size (the single-layer forward's 768-thread CTAs at N = 8192 spill 288 B here).
+template <int LOGN>
+using GeoHLC = GeoHL<LOGN>;
+
 template <int LOGN>
 __global__ void cascade_hl_pstash_kernel(const float* d, const float* bias, float4* out, int depth) {
-  using G = GeoHLF<LOGN>;
+  using G = GeoHLC<LOGN>;
   constexpr int T = G::T, N = G::NR;
   const int t = threadIdx.x;  // one group's threads (T <= 1024)
   const int l = blockIdx.x;
@@ -406,8 +411,8 @@ __global__ void cascade_hl_pstash_kernel(const float* d, const float* bias, floa
 }
 
 template <int LOGN>
-__global__ void ACDC_LB(GeoHLF<LOGN>) cascade_fwd_hl_kernel(CHParams p) {
-  using G = GeoHLF<LOGN>;
+__global__ void ACDC_LB(GeoHLC<LOGN>) cascade_fwd_hl_kernel(CHParams p) {
+  using G = GeoHLC<LOGN>;
   constexpr int T = G::T, N = G::NR;
   pdl_launch_dependents();
   extern __shared__ __align__(16) float smem_f[];
@@ -842,13 +847,12 @@ bool hl_launch_info(int logn, int kind, LaunchInfo* li) {
 // fn == nullptr where the size is not on the plan.
 template <int LOGN>
 static void hl_cascade_info(LaunchInfo* li) {
-  geom_hl<GeoHLF<LOGN>>(*li);
+  geom_hl<GeoHLC<LOGN>>(*li);
   li->fn = (const void*)cascade_fwd_hl_kernel<LOGN>;
-  li->scratch = GeoHLF<LOGN>::T;  // (threads of one group: the parameter re-layout kernel's block)
 }
 template <int LOGN>
 static void hl_cascade_pstash(const float* d, const float* bias, float4* out, int depth, cudaStream_t st) {
-  cascade_hl_pstash_kernel<LOGN><<<depth, GeoHLF<LOGN>::T, 0, st>>>(d, bias, out, depth);
+  cascade_hl_pstash_kernel<LOGN><<<depth, GeoHLC<LOGN>::T, 0, st>>>(d, bias, out, depth);
 }
 static void hl_cascade_pstash_launch(int logn, const float* d, const float* bias, float4* out, int depth,
                                      cudaStream_t st) {
