@@ -257,9 +257,19 @@ template <int LOGN>
 using GeoHLF = GeoHL<LOGN, hl_fwd_gpc<LOGN>()>;
 // d / bias of every thread's 8 spectral slots (32 bins) staged once per launch
 // in tensor memory, [slot] x (d0..d3, b0..b3), one tcgen05.ld per slot.
+#ifndef ACDC_HL_BWD_ASMEM  // 1: the backward stages its a quads in shared memory where they fit
+#define ACDC_HL_BWD_ASMEM 1  // A/B at N=4096: bwd -3%, step -1.6%
+#endif
+#ifndef ACDC_HL_FWD_ATM  // 1: the forward also stages its 8 a quads (32 floats) in TMEM (columns 64..95)
+#define ACDC_HL_FWD_ATM 1  // A/B at N=4096: fwd -3.8%, step -1.8%
+#endif
+template <int LOGN>
+__host__ __device__ constexpr int hl_fwd_ncol() {
+  return (ACDC_HL_FWD_ATM && (GeoHLF<LOGN>::CTA / 128) * 96 <= 512) ? 96 : 64;
+}
 template <int LOGN>
 __host__ __device__ constexpr int hl_fwd_cols() {
-  constexpr int need = (GeoHLF<LOGN>::CTA / 128) * 64;
+  constexpr int need = (GeoHLF<LOGN>::CTA / 128) * hl_fwd_ncol<LOGN>();
   return need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
 }
 // y = C3(d * C2(a * x) + bias) (layers.py:141-146), one row per group
@@ -288,7 +298,8 @@ __global__ void ACDC_LB(GeoHLF<LOGN>) acdc_fwd_hl_kernel(KParams p) {
   stage_tables_hl<G>(p.tab, smem_f, tw, cp, wn);
   if constexpr (!G::TW_SMEM) __syncthreads();
   tmem_fence_after();
-  const uint32_t ta = tmem_addr(tm_slot, warp, (warp >> 2) * 64);
+  constexpr int NCOLF = hl_fwd_ncol<LOGN>();
+  const uint32_t ta = tmem_addr(tm_slot, warp, (warp >> 2) * NCOLF);
   // programmatic dependent launch: the prologue above (constant tables, TMEM)
   // may overlap the previous kernel; d / bias, x, y and the h2 cache only after
   pdl_wait();
@@ -300,10 +311,48 @@ __global__ void ACDC_LB(GeoHLF<LOGN>) acdc_fwd_hl_kernel(KParams p) {
     for (int i = 0; i < 4; ++i) db[i] = __ldg(p.d + sl.b[i]), db[4 + i] = __ldg(p.bias + sl.b[i]);
     tmem_st8(ta + 8 * s, db);
   }
+  if constexpr (NCOLF == 96) {  // a at this thread's quads jsp + q*S
+    const float4* pa = reinterpret_cast<const float4*>(p.a) + fm.jsp;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float av[16];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float4 q4 = __ldg(pa + (4 * h + j) * FastMap<G>::S);
+        av[4 * j] = q4.x, av[4 * j + 1] = q4.y, av[4 * j + 2] = q4.z, av[4 * j + 3] = q4.w;
+      }
+      tmem_st16f(ta + 64 + 16 * h, av);
+    }
+  }
   for (int64_t r = c.gid; r < p.rows; r += c.gstride) {
     if (t == 0 && r + c.gstride < p.rows) prefetch_row_l2(p.x + (r + c.gstride) * p.ldx, G::NR);
     float2 v[16];
-    hl_load<G, true>(v, p.x + r * p.ldx, p.a, fm);
+    if constexpr (NCOLF == 96) {
+      float4 o[8];
+      const float4* px = reinterpret_cast<const float4*>(p.x + r * p.ldx) + fm.jsp;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o[q] = ld_row_f4(px + q * FastMap<G>::S);
+      float av[32];
+      {
+        float a0[16], a1[16];
+        tmem_ld16f(ta + 64, a0);
+        tmem_ld16f(ta + 80, a1);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) av[i] = a0[i], av[16 + i] = a1[i];
+      }
+      float2 snd[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 f = make_float4(o[q].x * av[4 * q], o[q].y * av[4 * q + 1], o[q].z * av[4 * q + 2],
+                                     o[q].w * av[4 * q + 3]);
+        v[q] = make_float2(f.x, f.z);
+        snd[q] = make_float2(f.w, f.y);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[15 - q] = fm.xor_shfl(snd[q]);
+    } else {
+      hl_load<G, true>(v, p.x + r * p.ldx, p.a, fm);
+    }
     fft_passes<G, 0, true>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
     {
       float2 w[8], gl[8], gh[8];
@@ -484,6 +533,12 @@ __host__ __device__ constexpr bool hl_tm_d() {  // d of the 32 slot bins also in
   return (GeoHLB<LOGN>::CTA / 128) * 128 <= 512;
 }
 template <int LOGN>
+__host__ __device__ constexpr bool hl_bwd_astash() {  // a quads staged in shared memory (where they fit)
+  // N <= 4096 (A/B: N=4096 step -1.6%; N=8192 / 16384 +5% / +4%: the larger stash costs L1 there)
+  return ACDC_HL_BWD_ASMEM && GeoHLB<LOGN>::T <= 128 &&
+         GeoHLB<LOGN>::SMEM_BYTES + 8 * GeoHLB<LOGN>::T * 16 + 1024 <= GeoHLB<LOGN>::SMEM_LIMIT;
+}
+template <int LOGN>
 __host__ __device__ constexpr bool hl_cta_red() {  // one gradient partial per CTA (all accumulators in TMEM)
 #ifdef ACDC_HL_NO_CTA_RED
   return GeoHLB<LOGN>::GPC == 1;
@@ -578,6 +633,17 @@ __global__ void ACDC_LB(GeoHLB<LOGN>) acdc_bwd_hl_kernel(KParams p) {
     }
   }
   pdl_wait();  // x, dy (maybe the forward's y) and the h2 cache are read from here on
+  // a at this thread's quads, [q][t] float4 after the tables / exchange buffers (shared by the groups)
+  constexpr bool AST = hl_bwd_astash<LOGN>();
+  float4* ast = reinterpret_cast<float4*>(smem_f + G::SMEM_BYTES / 4) + t;
+  if constexpr (AST) {
+    if (c.grp == 0) {
+      const float4* pa0 = reinterpret_cast<const float4*>(p.a) + fm.jsp;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) ast[q * T] = __ldg(pa0 + q * S);
+    }
+    __syncthreads();
+  }
   auto issue_dy = [&](int64_t row) {  // thread 0 of the group
     fence_proxy_async_smem();
     mbar_expect_tx(bar, (uint32_t)G::NR * 4u);
@@ -708,7 +774,7 @@ __global__ void ACDC_LB(GeoHLB<LOGN>) acdc_bwd_hl_kernel(KParams p) {
       }
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) po[q * S] = f4mul(__ldg(pa + q * S), g1[q]);
+    for (int q = 0; q < 8; ++q) po[q * S] = f4mul(AST ? ast[q * T] : __ldg(pa + q * S), g1[q]);
   }
   // Fewer partials where every accumulator is in TMEM: a "leader" group l < L
   // (L = max(1, 128 / T) groups cover the four TMEM lane quadrants) reads the
@@ -808,6 +874,7 @@ static void hl_info(int kind, LaunchInfo* li) {
       li->pdl = true;
 #endif
       li->max_per_sm = 512 / hl_cols<LOGN>();
+      if (hl_bwd_astash<LOGN>()) li->smem += 8 * GeoHLB<LOGN>::T * 16;  // the a stash
       if (hl_cta_red<LOGN>() && kind == 5) li->red_per_cta = hl_red_leaders<LOGN>();  // (cached backward)
       break;
     default: li->fn = nullptr;
