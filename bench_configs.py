@@ -90,9 +90,24 @@ def dense_step(n, B, dev, tf32):
     return step
 
 
-def c1(args, dev):
-    n, B = 256, 128
-    step, mode = layer_step(n, B, dev)
+def fused_step(n, B, dev):
+    """The fused small-batch step (functional.acdc_step: forward + backward +
+    gradient reduction in ONE launch for a dy known up front, as here)."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    x = torch.randn(B, n, device=dev, generator=g)
+    dy = torch.randn(B, n, device=dev, generator=g)
+    a = 1 + 0.1 * torch.randn(n, device=dev, generator=g)
+    d = 1 + 0.1 * torch.randn(n, device=dev, generator=g)
+    b = 0.1 * torch.randn(n, device=dev, generator=g)
+    gr = torch.zeros(3, n, device=dev)
+    y, dx = torch.empty_like(x), torch.empty_like(x)
+    F.prepare(n, dev)
+    assert B <= F.step_max_rows(n)
+    return lambda: F.acdc_step(x, dy, a, d, b, gr[0], gr[1], gr[2], accumulate=False, out_y=y, out_dx=dx)
+
+
+def graph_of(step):
     step()
     torch.cuda.synchronize()
     s = torch.cuda.Stream()
@@ -104,15 +119,28 @@ def c1(args, dev):
         with torch.cuda.graph(graph, stream=s):
             step()
     torch.cuda.synchronize()
-    ms_graph = timeit(graph.replay, args.steps * 10)
-    ms_eager = timeit(step, args.steps * 10)
+    return graph
+
+
+def c1(args, dev):
+    n, B = 256, 128
+    step, mode = layer_step(n, B, dev)
+    graph = graph_of(step)
+    ms_graph_sep = timeit(graph.replay, args.steps * 10)
+    ms_eager_sep = timeit(step, args.steps * 10)
+    fstep = fused_step(n, B, dev)
+    fgraph = graph_of(fstep)
+    ms_graph = timeit(fgraph.replay, args.steps * 10)
+    ms_eager = timeit(fstep, args.steps * 10)
     from bench import cpu_threads, reference_cpu
 
     thr = cpu_threads()
     rps_cpu, kind, sample, _, used = reference_cpu(n, min(thr, 8), B, seconds=3.0, warmup=1)
     rps = B / (ms_graph / 1e3)
-    return {"config": "C1 single ACDC layer N=256 batch 128 fwd+bwd", "mode": mode, "us_per_step_graph": ms_graph * 1e3,
-            "us_per_step_eager": ms_eager * 1e3, "rows_per_s": rps,
+    return {"config": "C1 single ACDC layer N=256 batch 128 fwd+bwd", "mode": "fused step (acdc_step_f32, 1 launch)",
+            "us_per_step_graph": ms_graph * 1e3, "us_per_step_eager": ms_eager * 1e3, "rows_per_s": rps,
+            "separate_calls": {"mode": mode, "launches": 3, "us_per_step_graph": ms_graph_sep * 1e3,
+                               "us_per_step_eager": ms_eager_sep * 1e3},
             "cpu_reference": {"rows_per_s": rps_cpu, "kind": kind, "threads": used, "sample": sample},
             "speedup_vs_cpu": rps / rps_cpu}
 

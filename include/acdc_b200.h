@@ -104,6 +104,20 @@ int acdc_bwd_cached_f32(const float* x, const float* dy, float* dx, const float*
                         size_t ws_bytes, int64_t rows, int32_t n, int64_t ldx, int64_t ldy, int64_t lddx,
                         acdc_stream_t stream);
 
+/* Fused single-layer step for small batches: the forward of acdc_fwd_f32 and
+ * the backward of acdc_bwd_f32 for an upstream gradient dy that does not depend
+ * on y (AcdcLayer.forward then AcdcLayer.backward, layers.py:141-156), in ONE
+ * kernel launch of one CTA, gradients written directly (no reduction launch).
+ * For batches whose step is launch-latency bound (BASELINE configs[0]: n = 256,
+ * 128 rows).  256 <= n <= 4096 and rows <= acdc_step_max_rows(n) (0 where the
+ * size has no fused step; ACDC_E_SIZE otherwise).  Same results as the pair of
+ * calls (bitwise while the separate backward runs one CTA); y, dx must not
+ * alias x, dy or each other. */
+int64_t acdc_step_max_rows(int32_t n);
+int acdc_step_f32(const float* x, const float* dy, float* y, float* dx, const float* a, const float* d,
+                  const float* bias, float* grad_a, float* grad_d, float* grad_bias, int accumulate, int64_t rows,
+                  int32_t n, int64_t ldx, int64_t ldy, int64_t ldo_y, int64_t ldo_dx, acdc_stream_t stream);
+
 /* Row-wise orthonormal DCT-II / DCT-III (the reference dct / idct). */
 /* ---- backward fused with the momentum-SGD step of the reference optimizer
  * (Sgd.step, training.py:58-98) applied to the layer's a, d, bias_d ----

@@ -56,6 +56,11 @@ SIGNATURES = {
         [_P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int, _P, ctypes.c_size_t, _I64, _I32, _I64, _I64, _I64, _P],
     ),
     "acdc_h2cache_bytes": (ctypes.c_size_t, [_I64, _I32]),
+    "acdc_step_max_rows": (_I64, [_I32]),
+    "acdc_step_f32": (
+        ctypes.c_int,
+        [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_int, _I64, _I32, _I64, _I64, _I64, _I64, _P],
+    ),
     "acdc_fwd_cache_f32": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I64, _I32, _I64, _I64, _P]),
     "acdc_bwd_cached_f32": (
         ctypes.c_int,

@@ -633,6 +633,198 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
   finish_partials<G>(p, smem_f);
 }
 
+// Fused single-layer step for small batches (BASELINE configs[0], C1: N = 256,
+// 128 rows): the forward y = C3(d * C2(a x) + bias) (layers.py:141-146) and
+// the backward for a given dy (layers.py:148-156) in ONE launch of ONE CTA,
+// gradients written directly (no partials, no reduction launch).  At these
+// sizes every launch costs more than its work (C1 ran three
+// dependent launches), so the step is one kernel: the recompute backward,
+// which computes h2 = C2(a x) anyway, plus the forward's inverse transform
+// (four packed FFTs per row pair, like the forward + cached backward).  Only
+// for a dy that does not depend on y (the C1 benchmark's synthetic dy, or a
+// caller that has its upstream gradient before the forward) — a training step
+// whose dy comes from y keeps the separate forward / backward launches.
+// Arithmetic per element is that of acdc_fwd_kernel and acdc_bwd_kernel<., false>,
+// and the gradient rounding that of a one-partial acdc_grad_reduce_kernel.
+#ifndef ACDC_STEP_MAX_ITERS  // row pairs per group in the one CTA
+#define ACDC_STEP_MAX_ITERS 4
+#endif
+template <int LOGN>
+__host__ __device__ constexpr bool step_ok() {
+  using G = GeoBwd<LOGN, false>;
+  return G::FP && cta_red<G>() && G::TW_SMEM && LOGN <= 12;
+}
+template <int LOGN>
+__global__ void ACDC_LB(GeoBwd<LOGN, false>) acdc_step_kernel(KParams p) {
+  using G = GeoBwd<LOGN, false>;
+  static_assert(step_ok<LOGN>(), "fused step: fast-pairing plan with on-chip group partials only");
+  constexpr int E = G::E;
+  constexpr int T = G::T;
+  constexpr int S = FastMap<G>::S;
+  extern __shared__ __align__(16) float smem_f[];
+  const auto c = group_ctx<G>();
+  const int t = c.t;
+  GroupSync<G> gs(c.grp);
+  float* gbase = smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS;
+  Xbuf<G> xb{gbase, 0};
+  float* sbase = gbase + G::NBUF * G::BUF_FLOATS;
+  float2* st_g3 = reinterpret_cast<float2*>(sbase) + t;             // [E][T]: g3, then the y spectrum
+  float2* st_ga2 = reinterpret_cast<float2*>(sbase + 2 * E * T) + t;  // [8][T]: grad_a partials
+  constexpr bool DST = bwd_dstash_bytes<LOGN, false>() > 0;
+  const float2* dst = reinterpret_cast<const float2*>(smem_f + G::SMEM_BYTES / 4) + t;
+  const FastMap<G> fm(t, gs.mask);
+  const float2 *tw, *cp;
+  pdl_wait();  // a / d / bias may come from the previous kernel (an SGD step)
+  if constexpr (DST) {  // group 0 fills; stage_tables' barrier publishes it
+    if (c.grp == 0) {
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        reinterpret_cast<float2*>(smem_f + G::SMEM_BYTES / 4)[t + s * T] =
+            make_float2(__ldg(fm.plo(p.d, s)), __ldg(fm.phi(p.d, s)));
+    }
+  }
+  stage_tables<G>(p.tab, smem_f, tw, cp);
+  pdl_launch_dependents();
+  float acc_d[E], acc_b[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    acc_d[i] = acc_b[i] = 0.f;
+    if (i < E / 2) st_ga2[i * T] = make_float2(0.f, 0.f);
+  }
+  const int64_t npairs = (p.rows + 1) >> 1;
+  const float2 chi = tab_load<G>(cp, G::N / 2);
+  for (int64_t rp = c.grp; rp < npairs; rp += G::GPC) {
+    const int64_t ra = 2 * rp;
+    const bool hasb = ra + 1 < p.rows;
+    const int64_t rb = hasb ? ra + 1 : ra;
+    const float* xa = p.x + ra * p.ldx;
+    const float* xbp = hasb ? p.x + rb * p.ldx : nullptr;
+    float2 v[16];
+    // g3 = C2(dy): grad_bias partial, stash
+    fp_load<G, false>(v, p.dy + ra * p.ldy, hasb ? p.dy + rb * p.ldy : nullptr, nullptr, fm);
+    fft_passes<G, 0>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
+    {
+      float2 w[8];
+      fp_partner<G>(v, w, fm);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        float2 gl, gh;
+        dct2_post(v[s], w[s], tab_load<G>(fm.plo(cp, s), 0), fm.special(s), chi, gl, gh);
+        acc_b[2 * s] += gl.x + gl.y;
+        acc_b[2 * s + 1] += gh.x + gh.y;
+        st_g3[(2 * s) * T] = gl;
+        st_g3[(2 * s + 1) * T] = gh;
+      }
+    }
+    // h2 = C2(a x): grad_d partial; Y = d g3 (-> g1) and d h2 + bias (-> y), both DCT-III pre-passed
+    fp_load<G, true>(v, xa, xbp, p.a, fm);
+    fft_passes<G, 0>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
+    {
+      float2 w[8], gl[8], gh[8];
+      fp_partner<G>(v, w, fm);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const float2 cs = tab_load<G>(fm.plo(cp, s), 0);
+        float2 hl, hh;
+        dct2_post(v[s], w[s], cs, fm.special(s), chi, hl, hh);
+        const float2 g3l = st_g3[(2 * s) * T], g3h = st_g3[(2 * s + 1) * T];
+        acc_d[2 * s] = fmaf(hl.x, g3l.x, fmaf(hl.y, g3l.y, acc_d[2 * s]));
+        acc_d[2 * s + 1] = fmaf(hh.x, g3h.x, fmaf(hh.y, g3h.y, acc_d[2 * s + 1]));
+        float dl, dh;
+        if constexpr (DST) {
+          const float2 dv = dst[s * T];
+          dl = dv.x, dh = dv.y;
+        } else {
+          dl = ld_plain(fm.plo(p.d, s)), dh = ld_plain(fm.phi(p.d, s));
+        }
+        const float bl = ld_plain(fm.plo(p.bias, s)), bh = ld_plain(fm.phi(p.bias, s));
+        dct3_pre(vmul(bc(dl), g3l), vmul(bc(dh), g3h), cs, fm.special(s), chi, gl[s], gh[s]);
+        float2 yl, yh;
+        dct3_pre(vfma(hl, bc(dl), bc(bl)), vfma(hh, bc(dh), bc(bh)), cs, fm.special(s), chi, yl, yh);
+        st_g3[(2 * s) * T] = yl;  // (this thread's own slots: no barrier)
+        st_g3[(2 * s + 1) * T] = yh;
+      }
+      fp_scatter<G>(gl, gh, v, fm);
+    }
+    // g1 = C3(d g3); dx = a g1; grad_a partial += x g1
+    fft_passes<G, 0>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
+    {
+      float2 ga[8], gb[8];
+      fp_out_pairs<G>(v, ga, gb, fm);
+      float2* oa = reinterpret_cast<float2*>(p.y + ra * p.ldo + 2 * fm.jsp);
+      float2* ob = reinterpret_cast<float2*>(p.y + rb * p.ldo + 2 * fm.jsp);
+      const float* pxa = xa + 2 * fm.jsp;
+      const float* pxb = p.x + rb * p.ldx + 2 * fm.jsp;
+      const float* pa = p.a + 2 * fm.jsp;
+      float2 xav[8], xbv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        xav[q] = ld_row_f2(pxa + 2 * q * S);
+        xbv[q] = hasb ? ld_row_f2(pxb + 2 * q * S) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float2 av = ld_f2(pa + 2 * q * S);
+        st_ga2[q * T] = cadd(st_ga2[q * T], vfma(gb[q], xbv[q], vmul(ga[q], xav[q])));
+        st_row_f2(oa + q * S, vmul(av, ga[q]));
+        if (hasb) st_row_f2(ob + q * S, vmul(av, gb[q]));
+      }
+    }
+    // y = C3(d h2 + bias)
+    {
+      float2 gl[8], gh[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        gl[s] = st_g3[(2 * s) * T];
+        gh[s] = st_g3[(2 * s + 1) * T];
+      }
+      fp_scatter<G>(gl, gh, v, fm);
+    }
+    fft_passes<G, 0>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
+    {
+      float2 oa[8], ob[8];
+      fp_out_pairs<G>(v, oa, ob, fm);
+      float2* ya = reinterpret_cast<float2*>(p.yf + ra * p.ldyf + 2 * fm.jsp);
+      float2* yb = reinterpret_cast<float2*>(p.yf + rb * p.ldyf + 2 * fm.jsp);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        st_row_f2(ya + q * S, oa[q]);
+        if (hasb) st_row_f2(yb + q * S, ob[q]);
+      }
+    }
+  }
+  // group partials -> the group's shared-memory region; the CTA sums them in
+  // group order (fp64) and writes the gradients (+= like the reference)
+  float2 gav[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) gav[q] = st_ga2[q * T];
+  gs.sync();  // the group's stash is read before its region is reused
+  float* w = gbase;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    w[2 * (fm.jsp + q * S)] = gav[q].x;
+    w[2 * (fm.jsp + q * S) + 1] = gav[q].y;
+  }
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    *fm.plo(w + G::N, s) = acc_d[2 * s];
+    *fm.phi(w + G::N, s) = acc_d[2 * s + 1];
+    *fm.plo(w + 2 * G::N, s) = acc_b[2 * s];
+    *fm.phi(w + 2 * G::N, s) = acc_b[2 * s + 1];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 3 * G::N; i += blockDim.x) {
+    double acc = 0.0;
+#pragma unroll 4
+    for (int g = 0; g < G::GPC; ++g) acc += (double)smem_f[G::TAB_FLOATS + g * G::GROUP_FLOATS + i];
+    const int comp = i / G::N, j = i - comp * G::N;
+    float* out = comp == 0 ? p.gout_a : (comp == 1 ? p.gout_d : p.gout_b);
+    double tot = (double)(float)acc;  // the one-partial reduction's rounding
+    if (p.accumulate) tot += (double)out[j];
+    out[j] = (float)tot;
+  }
+}
+
 // Cached-h2 backward with its per-thread gradient accumulators in TMEM
 // (tmem.cuh).  With the 48 accumulator floats out of the register file every
 // global load is issued one transform ahead of its use: the h2 block with dy
@@ -1810,6 +2002,35 @@ static int run(int kind, KParams p, int32_t n, cudaStream_t st) {
   return launch(li, grid, &p, st);
 }
 
+// Fused small-batch step (acdc_step_kernel): launch description for one CTA,
+// fn == nullptr where the size has no such kernel.
+template <int LOGN>
+static LaunchInfo step_info_t() {
+  LaunchInfo li;
+  if constexpr (LOGN >= 8 && step_ok<LOGN>()) {
+    using G = GeoBwd<LOGN, false>;
+    li.fn = (const void*)acdc_step_kernel<LOGN>;
+    geom<G>(li, 0);
+    li.smem += bwd_dstash_bytes<LOGN, false>();
+#ifndef ACDC_NO_PDL
+    li.pdl = true;
+#endif
+  }
+  return li;
+}
+static LaunchInfo step_info(int logn) {
+  switch (logn) {
+#ifndef ACDC_ONLY_LOGN
+    case 8: return step_info_t<8>();
+    case 9: return step_info_t<9>();
+    case 10: return step_info_t<10>();
+    case 11: return step_info_t<11>();
+    case 12: return step_info_t<12>();
+#endif
+    default: return LaunchInfo{};
+  }
+}
+
 }  // namespace acdc
 
 using namespace acdc;
@@ -2031,6 +2252,65 @@ int acdc_bwd_cached_f32(const float* x, const float* dy, float* dx, const float*
   if (acdc_h2cache_bytes(rows, n) == 0) return set_error(ACDC_E_SIZE, "the h2 cache needs n >= 256 and n <= 16384");
   return bwd_impl(K_BWD_H2, x, dy, dx, a, d, h2cache, grad_a, grad_d, grad_bias, accumulate, ws, ws_bytes, rows, n,
                   ldx, ldy, lddx, stream);
+}
+
+int64_t acdc_step_max_rows(int32_t n) {
+  int logn;
+  if (check_n(n, &logn)) return 0;
+  const LaunchInfo li = step_info(logn);
+  return li.fn ? (int64_t)2 * li.gpc * ACDC_STEP_MAX_ITERS : 0;
+}
+
+int acdc_step_f32(const float* x, const float* dy, float* y, float* dx, const float* a, const float* d,
+                  const float* bias, float* grad_a, float* grad_d, float* grad_bias, int accumulate, int64_t rows,
+                  int32_t n, int64_t ldx, int64_t ldy, int64_t ldo_y, int64_t ldo_dx, acdc_stream_t stream) {
+  int logn;
+  int rc = check_n(n, &logn);
+  if (rc) return rc;
+  const LaunchInfo li = step_info(logn);
+  if (!li.fn || rows > acdc_step_max_rows(n))
+    return set_error(ACDC_E_SIZE, "the fused step needs 256 <= n <= 4096 and rows <= acdc_step_max_rows(n)");
+  if ((rc = check_common(x, dx, rows, n, ldx, ldo_dx))) return rc;
+  if ((rc = check_common(x, y, rows, n, ldx, ldo_y))) return rc;
+  if (ldy < n) return ACDC_E_SHAPE;
+  if (!a || !d || !bias || !grad_a || !grad_d || !grad_bias || (rows > 0 && !dy)) return ACDC_E_NULL;
+  if (!pair_aligned(n, x, ldx) || !pair_aligned(n, dy, ldy) || !pair_aligned(n, dx, ldo_dx) ||
+      !pair_aligned(n, y, ldo_y) || !pair_aligned(n, a, 0))
+    return ACDC_E_ALIGN;
+  if (y == x || y == dy || dx == x || y == dx) return set_error(ACDC_E_SHAPE, "the fused step cannot write in place");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (rows == 0) {
+    if (!accumulate) {
+      cudaMemsetAsync(grad_a, 0, sizeof(float) * n, st);
+      cudaMemsetAsync(grad_d, 0, sizeof(float) * n, st);
+      cudaMemsetAsync(grad_bias, 0, sizeof(float) * n, st);
+    }
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
+  }
+  int64_t grid;
+  if ((rc = grid_for(li, 1, &grid))) return rc;  // (sets the smem attribute; one CTA)
+  Tables tb;
+  if ((rc = get_tables(logn, &tb))) return rc;
+  KParams p{};
+  p.x = x;
+  p.dy = dy;
+  p.y = dx;
+  p.yf = y;
+  p.a = a;
+  p.d = d;
+  p.bias = bias;
+  p.gout_a = grad_a;
+  p.gout_d = grad_d;
+  p.gout_b = grad_bias;
+  p.accumulate = accumulate;
+  p.tab = tb.tab;
+  p.rows = rows;
+  p.ldx = ldx;
+  p.ldy = ldy;
+  p.ldo = ldo_dx;
+  p.ldyf = ldo_y;
+  return launch(li, 1, &p, st);
 }
 
 int cascade_gather_supported(int32_t n) {

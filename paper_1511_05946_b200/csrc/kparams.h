@@ -31,6 +31,13 @@ struct KParams {
   float* ws2;
   int epi_relu2;
   int64_t ldx2;
+  // fused single-layer step (acdc_step_kernel): the forward's y and the final gradients (written directly)
+  float* yf;
+  float* gout_a;
+  float* gout_d;
+  float* gout_b;
+  int accumulate;
+  int64_t ldyf;
   int64_t rows;
   int64_t ldx, ldy, ldo;
 };

@@ -23,6 +23,8 @@ __all__ = [
     "acdc_forward",
     "acdc_backward",
     "acdc_backward_sgd",
+    "acdc_step",
+    "step_max_rows",
     "dct",
     "fft",
     "ifft",
@@ -148,6 +150,45 @@ def acdc_forward(x: torch.Tensor, a: torch.Tensor, d: torch.Tensor, bias: torch.
                                         _ld(x, n), _ld(y, n), _stream(x))
         _lib.check(rc)
     return y
+
+
+def step_max_rows(n: int) -> int:
+    """Largest batch :func:`acdc_step` runs as one fused launch at size n (0: none)."""
+    return int(_lib.load().acdc_step_max_rows(int(n)))
+
+
+def acdc_step(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, d: torch.Tensor, bias: torch.Tensor,
+              grad_a: torch.Tensor, grad_d: torch.Tensor, grad_bias: torch.Tensor, accumulate: bool = True,
+              out_y=None, out_dx=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Forward and backward of one layer for an upstream gradient ``dy`` known
+    before the forward (AcdcLayer.forward then .backward, layers.py:141-156):
+    returns (y, dx) and updates the gradients like :func:`acdc_backward`.
+
+    Up to :func:`step_max_rows` rows (small batches, 256 <= n <= 4096) this is
+    ONE kernel launch (forward, backward and the gradient reduction in one
+    CTA); larger batches run :func:`acdc_forward` + :func:`acdc_backward`."""
+    n = a.shape[0]
+    x = _rows2d(x, n)
+    dy = _rows2d(dy, n, "grad_y")
+    if dy.shape[0] != x.shape[0]:
+        raise ValueError(f"grad_y has {dy.shape[0]} rows, input had {x.shape[0]}")
+    rows = x.shape[0]
+    if rows > step_max_rows(n):
+        y = acdc_forward(x, a, d, bias, out=out_y)
+        return y, acdc_backward(x, dy, a, d, grad_a, grad_d, grad_bias, accumulate=accumulate, out=out_dx)
+    dev = x.device
+    a, d, bias = (_vec(v, n, dev, nm) for v, nm in ((a, "a"), (d, "d"), (bias, "bias")))
+    for g in (grad_a, grad_d, grad_bias):
+        if g.device != dev or g.dtype != torch.float32 or not g.is_contiguous() or g.shape != (n,):
+            raise ValueError("gradient buffers must be contiguous fp32 (n,) tensors on the input device")
+    y = torch.empty_like(x, memory_format=torch.contiguous_format) if out_y is None else _check_out(out_y, x, "out_y")
+    dx = torch.empty_like(x, memory_format=torch.contiguous_format) if out_dx is None else _check_out(out_dx, x, "out_dx")
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        _lib.check(lib.acdc_step_f32(_ptr(x), _ptr(dy), _ptr(y), _ptr(dx), _ptr(a), _ptr(d), _ptr(bias), _ptr(grad_a),
+                                     _ptr(grad_d), _ptr(grad_bias), 1 if accumulate else 0, rows, n, _ld(x, n),
+                                     _ld(dy, n), _ld(y, n), _ld(dx, n), _stream(x)))
+    return y, dx
 
 
 def acdc_backward(

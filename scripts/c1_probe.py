@@ -59,6 +59,9 @@ def main():
            "step_us": graph_us(lambda: (fwd(), bwd())),
            "noop_kernel_us": graph_us(lambda: empty.add_(1.0)),
            "bwd_launches": F._lib.load().acdc_bwd_launch_count(rows, n, 1 if hc is not None else 0)}
+    if rows <= F.step_max_rows(n):  # the fused one-launch step (acdc_step_f32)
+        res["fused_step_us"] = graph_us(lambda: F.acdc_step(x, dy, a, d, b, g[0], g[1], g[2], accumulate=False,
+                                                           out_y=y, out_dx=dx))
     print(json.dumps(res), flush=True)
 
 

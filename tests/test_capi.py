@@ -86,3 +86,20 @@ def test_sgd_entry_validation(lib):
     st.velocity[1] = None
     assert f(None, None, None, None, None, 0, None, None, None, 0, ctypes.byref(st), None, 0, 4, 256, 256, 256, 256,
              None) == _lib.ACDC_E_NULL
+
+
+def test_step_entry_limits(lib):
+    """The fused small-batch step: sizes and row limits (host logic, no GPU)."""
+    from paper_1511_05946_b200 import _lib
+
+    assert lib.acdc_step_max_rows(128) == 0 and lib.acdc_step_max_rows(8192) == 0
+    assert lib.acdc_step_max_rows(256) >= 128  # C1 (n = 256, 128 rows) is one launch
+    for n in (256, 512, 1024, 2048, 4096):
+        assert lib.acdc_step_max_rows(n) > 0
+    rc = lib.acdc_step_f32(None, None, None, None, None, None, None, None, None, None, 0, 4, 128, 128, 128, 128, 128,
+                           None)
+    assert rc == _lib.ACDC_E_SIZE
+    big = lib.acdc_step_max_rows(256) + 1
+    rc = lib.acdc_step_f32(None, None, None, None, None, None, None, None, None, None, 0, big, 256, 256, 256, 256,
+                           256, None)
+    assert rc == _lib.ACDC_E_SIZE
