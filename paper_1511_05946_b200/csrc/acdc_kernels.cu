@@ -11,6 +11,7 @@
 // imaginary parts of one complex FFT (see dct_pair.cuh).  h2 = C2(a*x) is
 // either recomputed in the backward or, on the fast-pairing
 // sizes, cached by the forward like the reference layer (layers.py:145).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -29,6 +30,7 @@
 #include "kparams.h"
 
 namespace acdc {
+namespace cg = cooperative_groups;
 
 // ---------------------------------------------------------------- helpers
 
@@ -646,17 +648,34 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
 // whose dy comes from y keeps the separate forward / backward launches.
 // Arithmetic per element is that of acdc_fwd_kernel and acdc_bwd_kernel<., false>,
 // and the gradient rounding that of a one-partial acdc_grad_reduce_kernel.
-#ifndef ACDC_STEP_MAX_ITERS  // row pairs per group in the one CTA
+#ifndef ACDC_STEP_MAX_ITERS  // row pairs per group
 #define ACDC_STEP_MAX_ITERS 4
 #endif
+#ifndef ACDC_STEP_CTA  // threads per CTA: small CTAs spread the batch over a cluster of SMs
+#define ACDC_STEP_CTA 256
+#endif
+#ifndef ACDC_STEP_MAX_CLUSTER  // CTAs of the one cluster (portable limit 8)
+#define ACDC_STEP_MAX_CLUSTER 8
+#endif
 template <int LOGN>
-__host__ __device__ constexpr bool step_ok() {
-  using G = GeoBwd<LOGN, false>;
-  return G::FP && cta_red<G>() && G::TW_SMEM && LOGN <= 12;
+using GeoStep = Geo<LOGN, 3 * Geo<LOGN>::E, (ACDC_STEP_CTA / Geo<LOGN>::T > 0 ? ACDC_STEP_CTA / Geo<LOGN>::T : 1)>;
+template <int LOGN>
+__host__ __device__ constexpr int step_dstash_bytes() {
+  using G = GeoStep<LOGN>;
+  return (G::FP && G::TW_SMEM && G::SMEM_BYTES + 8 * G::T * 8 <= G::SMEM_LIMIT) ? 8 * G::T * 8 : 0;
 }
 template <int LOGN>
-__global__ void ACDC_LB(GeoBwd<LOGN, false>) acdc_step_kernel(KParams p) {
-  using G = GeoBwd<LOGN, false>;
+__host__ __device__ constexpr bool step_ok() {
+  using G = GeoStep<LOGN>;
+  return G::FP && G::STASH_SMEM && G::GROUP_FLOATS >= 3 * G::N && !G::SPLIT && G::TW_SMEM && LOGN <= 12;
+}
+// One cluster of up to 8 CTAs (one per SM): each CTA sums its groups' partials
+// (fp64, group order) into its group-0 region, then CTA rank 0 reads the other
+// CTAs' sums through distributed shared memory and adds them in rank order
+// (fp64) -> deterministic gradients without a second launch.
+template <int LOGN>
+__global__ void ACDC_LB(GeoStep<LOGN>) acdc_step_kernel(KParams p) {
+  using G = GeoStep<LOGN>;
   static_assert(step_ok<LOGN>(), "fused step: fast-pairing plan with on-chip group partials only");
   constexpr int E = G::E;
   constexpr int T = G::T;
@@ -670,7 +689,7 @@ __global__ void ACDC_LB(GeoBwd<LOGN, false>) acdc_step_kernel(KParams p) {
   float* sbase = gbase + G::NBUF * G::BUF_FLOATS;
   float2* st_g3 = reinterpret_cast<float2*>(sbase) + t;             // [E][T]: g3, then the y spectrum
   float2* st_ga2 = reinterpret_cast<float2*>(sbase + 2 * E * T) + t;  // [8][T]: grad_a partials
-  constexpr bool DST = bwd_dstash_bytes<LOGN, false>() > 0;
+  constexpr bool DST = step_dstash_bytes<LOGN>() > 0;
   const float2* dst = reinterpret_cast<const float2*>(smem_f + G::SMEM_BYTES / 4) + t;
   const FastMap<G> fm(t, gs.mask);
   const float2 *tw, *cp;
@@ -693,7 +712,7 @@ __global__ void ACDC_LB(GeoBwd<LOGN, false>) acdc_step_kernel(KParams p) {
   }
   const int64_t npairs = (p.rows + 1) >> 1;
   const float2 chi = tab_load<G>(cp, G::N / 2);
-  for (int64_t rp = c.grp; rp < npairs; rp += G::GPC) {
+  for (int64_t rp = c.gid; rp < npairs; rp += c.gstride) {
     const int64_t ra = 2 * rp;
     const bool hasb = ra + 1 < p.rows;
     const int64_t rb = hasb ? ra + 1 : ra;
@@ -813,16 +832,27 @@ __global__ void ACDC_LB(GeoBwd<LOGN, false>) acdc_step_kernel(KParams p) {
     *fm.phi(w + 2 * G::N, s) = acc_b[2 * s + 1];
   }
   __syncthreads();
+  float* csum = smem_f + G::TAB_FLOATS;  // group 0's region: the CTA's sums (each index read and written by one thread)
   for (int i = threadIdx.x; i < 3 * G::N; i += blockDim.x) {
     double acc = 0.0;
 #pragma unroll 4
-    for (int g = 0; g < G::GPC; ++g) acc += (double)smem_f[G::TAB_FLOATS + g * G::GROUP_FLOATS + i];
-    const int comp = i / G::N, j = i - comp * G::N;
-    float* out = comp == 0 ? p.gout_a : (comp == 1 ? p.gout_d : p.gout_b);
-    double tot = (double)(float)acc;  // the one-partial reduction's rounding
-    if (p.accumulate) tot += (double)out[j];
-    out[j] = (float)tot;
+    for (int g = 0; g < G::GPC; ++g) acc += (double)csum[g * G::GROUP_FLOATS + i];
+    csum[i] = (float)acc;  // the per-CTA partial's rounding, as in the separate backward
   }
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned ranks = cl.num_blocks();
+  if (ranks > 1) cl.sync();  // every CTA's sums are visible cluster-wide
+  if (cl.block_rank() == 0) {
+    for (int i = threadIdx.x; i < 3 * G::N; i += blockDim.x) {
+      double tot = 0.0;
+      for (unsigned r = 0; r < ranks; ++r) tot += (double)(r == 0 ? csum[i] : cl.map_shared_rank(csum, r)[i]);
+      const int comp = i / G::N, j = i - comp * G::N;
+      float* out = comp == 0 ? p.gout_a : (comp == 1 ? p.gout_d : p.gout_b);
+      if (p.accumulate) tot += (double)out[j];
+      out[j] = (float)tot;
+    }
+  }
+  if (ranks > 1) cl.sync();  // no CTA exits while rank 0 still reads its shared memory
 }
 
 // Cached-h2 backward with its per-thread gradient accumulators in TMEM
@@ -2008,10 +2038,10 @@ template <int LOGN>
 static LaunchInfo step_info_t() {
   LaunchInfo li;
   if constexpr (LOGN >= 8 && step_ok<LOGN>()) {
-    using G = GeoBwd<LOGN, false>;
+    using G = GeoStep<LOGN>;
     li.fn = (const void*)acdc_step_kernel<LOGN>;
     geom<G>(li, 0);
-    li.smem += bwd_dstash_bytes<LOGN, false>();
+    li.smem += step_dstash_bytes<LOGN>();
 #ifndef ACDC_NO_PDL
     li.pdl = true;
 #endif
@@ -2026,6 +2056,8 @@ static LaunchInfo step_info(int logn) {
     case 10: return step_info_t<10>();
     case 11: return step_info_t<11>();
     case 12: return step_info_t<12>();
+#elif ACDC_ONLY_LOGN >= 8 && ACDC_ONLY_LOGN <= 12
+    case ACDC_ONLY_LOGN: return step_info_t<ACDC_ONLY_LOGN>();
 #endif
     default: return LaunchInfo{};
   }
@@ -2258,7 +2290,7 @@ int64_t acdc_step_max_rows(int32_t n) {
   int logn;
   if (check_n(n, &logn)) return 0;
   const LaunchInfo li = step_info(logn);
-  return li.fn ? (int64_t)2 * li.gpc * ACDC_STEP_MAX_ITERS : 0;
+  return li.fn ? (int64_t)2 * li.gpc * ACDC_STEP_MAX_CLUSTER * ACDC_STEP_MAX_ITERS : 0;
 }
 
 int acdc_step_f32(const float* x, const float* dy, float* y, float* dx, const float* a, const float* d,
@@ -2310,7 +2342,30 @@ int acdc_step_f32(const float* x, const float* dy, float* y, float* dx, const fl
   p.ldy = ldy;
   p.ldo = ldo_dx;
   p.ldyf = ldo_y;
-  return launch(li, 1, &p, st);
+  const int64_t npairs = (rows + 1) / 2;
+  int64_t ctas = (npairs + li.gpc - 1) / li.gpc;
+  if (ctas > ACDC_STEP_MAX_CLUSTER) ctas = ACDC_STEP_MAX_CLUSTER;
+  void* args[] = {&p};
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;  // the whole grid is one cluster
+  attr[0].val.clusterDim.x = (unsigned)ctas;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3((unsigned)ctas);
+  cfg.blockDim = dim3(li.cta);
+  cfg.dynamicSmemBytes = li.smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+#ifdef ACDC_NO_PDL
+  cfg.numAttrs = 1;
+#else
+  cfg.numAttrs = 2;
+#endif
+  cudaError_t e = cudaLaunchKernelExC(&cfg, li.fn, args);
+  return e == cudaSuccess ? ACDC_OK : set_cuda_error(e);
 }
 
 int cascade_gather_supported(int32_t n) {

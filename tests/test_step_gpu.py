@@ -2,20 +2,41 @@
 gradient reduction in one launch) vs the fp64 oracle and vs the separate
 forward / backward kernels (layers.py:141-156).
 
-Tolerances as tests/test_parity_gpu.py.  Where the separate
-recompute backward also runs one CTA the gradients and dx must be bitwise
-equal (same arithmetic, same one-partial rounding)."""
+Tolerances as tests/test_parity_gpu.py.  The step runs one
+cluster of up to 8 CTAs (gradients summed over distributed shared memory), so
+the cases cover one CTA, several CTAs, a full cluster and several row pairs
+per group."""
 
 import numpy as np
 import pytest
 import torch
 
 from oracle import acdc_oracle as O
-from tests.test_parity_gpu import assert_close_grad, assert_close_rows, f32, t32
-
 pytestmark = pytest.mark.gpu
 
 DEV = "cuda"
+
+
+def t32(a):
+    return torch.as_tensor(np.asarray(a, dtype=np.float32), device=DEV)
+
+
+def f32(rng, *shape, mean=0.0, std=1.0):
+    return (mean + std * rng.standard_normal(shape)).astype(np.float32)
+
+
+def assert_close_rows(mine, ref, n, what):
+    mine = mine.detach().cpu().double().numpy()
+    tol = O.fp32_tolerance(n, ref)
+    err = float(np.abs(mine - ref).max()) if ref.size else 0.0
+    assert err <= tol, f"{what}: max err {err:.3e} > tol {tol:.3e} (N={n})"
+
+
+def assert_close_grad(mine, ref, n, rows, what):
+    mine = mine.detach().cpu().double().numpy()
+    tol = O.grad_tolerance(n, rows, ref)
+    err = float(np.abs(mine - ref).max())
+    assert err <= tol, f"{what}: max err {err:.3e} > tol {tol:.3e} (N={n}, B={rows})"
 
 
 def _inputs(n, rows, seed):
@@ -26,9 +47,10 @@ def _inputs(n, rows, seed):
     return x, dy, a, d, b
 
 
-@pytest.mark.parametrize("n,rows", [(256, 128), (256, 1), (256, 2), (256, 3), (256, 64), (256, 255), (256, 256),
-                                    (512, 128), (512, 77), (1024, 64), (1024, 5), (2048, 32), (2048, 9),
-                                    (4096, 16), (4096, 7)])
+@pytest.mark.parametrize("n,rows", [(256, 128), (256, 1), (256, 2), (256, 3), (256, 32), (256, 33), (256, 255),
+                                    (256, 256), (256, 257), (256, 1000), (256, 1024), (512, 128), (512, 77),
+                                    (512, 512), (1024, 64), (1024, 5), (1024, 256), (2048, 32), (2048, 9),
+                                    (2048, 128), (4096, 16), (4096, 7), (4096, 64)])
 def test_step_vs_oracle(n, rows):
     from paper_1511_05946_b200 import functional as F
 
@@ -48,8 +70,9 @@ def test_step_vs_oracle(n, rows):
 
 
 @pytest.mark.parametrize("n,rows", [(256, 64), (256, 33), (512, 32), (1024, 16), (2048, 8), (4096, 4)])
-def test_step_bitwise_vs_separate_one_cta(n, rows):
-    """Rows within one CTA of the separate recompute backward: identical bits."""
+def test_step_vs_separate(n, rows):
+    """Same arithmetic as the separate kernels; only the grouping of the
+    gradient partial sums differs (CTA sizes)."""
     from paper_1511_05946_b200 import functional as F
 
     x, dy, a, d, b = map(t32, _inputs(n, rows, 9100 + n))
@@ -59,9 +82,13 @@ def test_step_bitwise_vs_separate_one_cta(n, rows):
     y2 = F.acdc_forward(x, a, d, b)
     dx2 = F.acdc_backward(x, dy, a, d, *g2, accumulate=True)
     torch.cuda.synchronize()
-    assert torch.equal(dx1, dx2)
+    if n <= 512:  # the separate backward is the row-pair recompute kernel: identical per-element arithmetic
+        assert torch.equal(dx1, dx2)
+    else:  # the separate path runs the half-length plan from n = 1024
+        assert float((dx1 - dx2).abs().max()) <= O.fp32_tolerance(n, dx2.double().cpu().numpy())
     for u, v in zip(g1, g2):
-        assert torch.equal(u, v)
+        gt = O.grad_tolerance(n, rows, v.double().cpu().numpy())
+        assert float((u - v).abs().max()) <= gt
     tol = O.fp32_tolerance(n, y2.double().cpu().numpy())
     assert float((y1 - y2).abs().max()) <= tol  # (the forward kernel's exchange layout may differ)
 
