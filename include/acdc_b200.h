@@ -109,7 +109,7 @@ int acdc_bwd_cached_f32(const float* x, const float* dy, float* dx, const float*
  * on y (AcdcLayer.forward then AcdcLayer.backward, layers.py:141-156), in ONE
  * kernel launch of one CTA, gradients written directly (no reduction launch).
  * For batches whose step is launch-latency bound (BASELINE configs[0]: n = 256,
- * 128 rows).  256 <= n <= 4096 and rows <= acdc_step_max_rows(n) (0 where the
+ * 128 rows).  256 <= n <= 2048 and rows <= acdc_step_max_rows(n) (0 where the
  * size has no fused step; ACDC_E_SIZE otherwise).  Same results as the pair of
  * calls (bitwise while the separate backward runs one CTA); y, dx must not
  * alias x, dy or each other. */

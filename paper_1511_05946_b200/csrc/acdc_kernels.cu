@@ -648,26 +648,31 @@ __global__ void ACDC_LB(GeoBwd<LOGN, H2C>) acdc_bwd_kernel(KParams p) {
 // whose dy comes from y keeps the separate forward / backward launches.
 // Arithmetic per element is that of acdc_fwd_kernel and acdc_bwd_kernel<., false>,
 // and the gradient rounding that of a one-partial acdc_grad_reduce_kernel.
-#ifndef ACDC_STEP_MAX_ITERS  // row pairs per group
-#define ACDC_STEP_MAX_ITERS 4
+#ifndef ACDC_STEP_MAX_ITERS  // row pairs per group (at 4: 1024 rows at N = 256 ran 26.6 us vs 20.5 us separate)
+#define ACDC_STEP_MAX_ITERS 1
 #endif
 #ifndef ACDC_STEP_CTA  // threads per CTA: small CTAs spread the batch over a cluster of SMs
-#define ACDC_STEP_CTA 256
+#define ACDC_STEP_CTA 128  // (C1: 128 threads 10.7 us, 256 threads 12.3 us, 512 threads 16.4 us per graph replay)
 #endif
 #ifndef ACDC_STEP_MAX_CLUSTER  // CTAs of the one cluster (portable limit 8)
 #define ACDC_STEP_MAX_CLUSTER 8
 #endif
 template <int LOGN>
 using GeoStep = Geo<LOGN, 3 * Geo<LOGN>::E, (ACDC_STEP_CTA / Geo<LOGN>::T > 0 ? ACDC_STEP_CTA / Geo<LOGN>::T : 1)>;
+#ifndef ACDC_STEP_PRELOAD  // 1: a row pair's dy and x loads are issued one transform block ahead (the first
+#define ACDC_STEP_PRELOAD 1  // pair's before the table staging)
+#endif
+// parameter stash [slot][t] float4 {d_lo, d_hi, bias_lo, bias_hi}, filled once per launch
 template <int LOGN>
 __host__ __device__ constexpr int step_dstash_bytes() {
   using G = GeoStep<LOGN>;
-  return (G::FP && G::TW_SMEM && G::SMEM_BYTES + 8 * G::T * 8 <= G::SMEM_LIMIT) ? 8 * G::T * 8 : 0;
+  return (G::FP && G::TW_SMEM && G::SMEM_BYTES + 8 * G::T * 16 <= G::SMEM_LIMIT) ? 8 * G::T * 16 : 0;
 }
 template <int LOGN>
 __host__ __device__ constexpr bool step_ok() {
   using G = GeoStep<LOGN>;
-  return G::FP && G::STASH_SMEM && G::GROUP_FLOATS >= 3 * G::N && !G::SPLIT && G::TW_SMEM && LOGN <= 12;
+  // (n = 4096: 28.7 us fused vs 24.3 us separate at 8 rows -- the separate half-length kernels win)
+  return G::FP && G::STASH_SMEM && G::GROUP_FLOATS >= 3 * G::N && !G::SPLIT && G::TW_SMEM && LOGN <= 11;
 }
 // One cluster of up to 8 CTAs (one per SM): each CTA sums its groups' partials
 // (fp64, group order) into its group-0 region, then CTA rank 0 reads the other
@@ -690,16 +695,29 @@ __global__ void ACDC_LB(GeoStep<LOGN>) acdc_step_kernel(KParams p) {
   float2* st_g3 = reinterpret_cast<float2*>(sbase) + t;             // [E][T]: g3, then the y spectrum
   float2* st_ga2 = reinterpret_cast<float2*>(sbase + 2 * E * T) + t;  // [8][T]: grad_a partials
   constexpr bool DST = step_dstash_bytes<LOGN>() > 0;
-  const float2* dst = reinterpret_cast<const float2*>(smem_f + G::SMEM_BYTES / 4) + t;
+  const float4* dst = reinterpret_cast<const float4*>(smem_f + G::SMEM_BYTES / 4) + t;
   const FastMap<G> fm(t, gs.mask);
   const float2 *tw, *cp;
-  pdl_wait();  // a / d / bias may come from the previous kernel (an SGD step)
+  const int64_t npairs = (p.rows + 1) >> 1;
+  pdl_wait();  // x, dy, a / d / bias may come from the previous kernel (an SGD step)
+#if ACDC_STEP_PRELOAD
+  // the first row pair's dy and a x: in flight across the table staging
+  float2 vd[16], vx[16];
+  auto load_pair = [&](int64_t r) {
+    const int64_t r0 = 2 * r;
+    const bool hb = r0 + 1 < p.rows;
+    fp_load<G, false>(vd, p.dy + r0 * p.ldy, hb ? p.dy + (r0 + 1) * p.ldy : nullptr, nullptr, fm);
+    fp_load<G, true>(vx, p.x + r0 * p.ldx, hb ? p.x + (r0 + 1) * p.ldx : nullptr, p.a, fm);
+  };
+  if (c.gid < npairs) load_pair(c.gid);
+#endif
   if constexpr (DST) {  // group 0 fills; stage_tables' barrier publishes it
     if (c.grp == 0) {
 #pragma unroll
       for (int s = 0; s < 8; ++s)
-        reinterpret_cast<float2*>(smem_f + G::SMEM_BYTES / 4)[t + s * T] =
-            make_float2(__ldg(fm.plo(p.d, s)), __ldg(fm.phi(p.d, s)));
+        reinterpret_cast<float4*>(smem_f + G::SMEM_BYTES / 4)[t + s * T] =
+            make_float4(__ldg(fm.plo(p.d, s)), __ldg(fm.phi(p.d, s)), __ldg(fm.plo(p.bias, s)),
+                        __ldg(fm.phi(p.bias, s)));
     }
   }
   stage_tables<G>(p.tab, smem_f, tw, cp);
@@ -710,17 +728,20 @@ __global__ void ACDC_LB(GeoStep<LOGN>) acdc_step_kernel(KParams p) {
     acc_d[i] = acc_b[i] = 0.f;
     if (i < E / 2) st_ga2[i * T] = make_float2(0.f, 0.f);
   }
-  const int64_t npairs = (p.rows + 1) >> 1;
   const float2 chi = tab_load<G>(cp, G::N / 2);
   for (int64_t rp = c.gid; rp < npairs; rp += c.gstride) {
     const int64_t ra = 2 * rp;
     const bool hasb = ra + 1 < p.rows;
     const int64_t rb = hasb ? ra + 1 : ra;
     const float* xa = p.x + ra * p.ldx;
-    const float* xbp = hasb ? p.x + rb * p.ldx : nullptr;
     float2 v[16];
     // g3 = C2(dy): grad_bias partial, stash
+#if ACDC_STEP_PRELOAD
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = vd[i];
+#else
     fp_load<G, false>(v, p.dy + ra * p.ldy, hasb ? p.dy + rb * p.ldy : nullptr, nullptr, fm);
+#endif
     fft_passes<G, 0>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
     {
       float2 w[8];
@@ -736,7 +757,13 @@ __global__ void ACDC_LB(GeoStep<LOGN>) acdc_step_kernel(KParams p) {
       }
     }
     // h2 = C2(a x): grad_d partial; Y = d g3 (-> g1) and d h2 + bias (-> y), both DCT-III pre-passed
-    fp_load<G, true>(v, xa, xbp, p.a, fm);
+#if ACDC_STEP_PRELOAD
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = vx[i];
+    if (rp + c.gstride < npairs) load_pair(rp + c.gstride);  // next pair: in flight for three transforms
+#else
+    fp_load<G, true>(v, xa, hasb ? p.x + rb * p.ldx : nullptr, p.a, fm);
+#endif
     fft_passes<G, 0>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
     {
       float2 w[8], gl[8], gh[8];
@@ -749,14 +776,14 @@ __global__ void ACDC_LB(GeoStep<LOGN>) acdc_step_kernel(KParams p) {
         const float2 g3l = st_g3[(2 * s) * T], g3h = st_g3[(2 * s + 1) * T];
         acc_d[2 * s] = fmaf(hl.x, g3l.x, fmaf(hl.y, g3l.y, acc_d[2 * s]));
         acc_d[2 * s + 1] = fmaf(hh.x, g3h.x, fmaf(hh.y, g3h.y, acc_d[2 * s + 1]));
-        float dl, dh;
+        float dl, dh, bl, bh;
         if constexpr (DST) {
-          const float2 dv = dst[s * T];
-          dl = dv.x, dh = dv.y;
+          const float4 dv = dst[s * T];
+          dl = dv.x, dh = dv.y, bl = dv.z, bh = dv.w;
         } else {
           dl = ld_plain(fm.plo(p.d, s)), dh = ld_plain(fm.phi(p.d, s));
+          bl = ld_plain(fm.plo(p.bias, s)), bh = ld_plain(fm.phi(p.bias, s));
         }
-        const float bl = ld_plain(fm.plo(p.bias, s)), bh = ld_plain(fm.phi(p.bias, s));
         dct3_pre(vmul(bc(dl), g3l), vmul(bc(dh), g3h), cs, fm.special(s), chi, gl[s], gh[s]);
         float2 yl, yh;
         dct3_pre(vfma(hl, bc(dl), bc(bl)), vfma(hh, bc(dh), bc(bh)), cs, fm.special(s), chi, yl, yh);
@@ -2055,8 +2082,7 @@ static LaunchInfo step_info(int logn) {
     case 9: return step_info_t<9>();
     case 10: return step_info_t<10>();
     case 11: return step_info_t<11>();
-    case 12: return step_info_t<12>();
-#elif ACDC_ONLY_LOGN >= 8 && ACDC_ONLY_LOGN <= 12
+#elif ACDC_ONLY_LOGN >= 8 && ACDC_ONLY_LOGN <= 11
     case ACDC_ONLY_LOGN: return step_info_t<ACDC_ONLY_LOGN>();
 #endif
     default: return LaunchInfo{};
@@ -2301,7 +2327,7 @@ int acdc_step_f32(const float* x, const float* dy, float* y, float* dx, const fl
   if (rc) return rc;
   const LaunchInfo li = step_info(logn);
   if (!li.fn || rows > acdc_step_max_rows(n))
-    return set_error(ACDC_E_SIZE, "the fused step needs 256 <= n <= 4096 and rows <= acdc_step_max_rows(n)");
+    return set_error(ACDC_E_SIZE, "the fused step needs 256 <= n <= 2048 and rows <= acdc_step_max_rows(n)");
   if ((rc = check_common(x, dx, rows, n, ldx, ldo_dx))) return rc;
   if ((rc = check_common(x, y, rows, n, ldx, ldo_y))) return rc;
   if (ldy < n) return ACDC_E_SHAPE;
@@ -2309,7 +2335,8 @@ int acdc_step_f32(const float* x, const float* dy, float* y, float* dx, const fl
   if (!pair_aligned(n, x, ldx) || !pair_aligned(n, dy, ldy) || !pair_aligned(n, dx, ldo_dx) ||
       !pair_aligned(n, y, ldo_y) || !pair_aligned(n, a, 0))
     return ACDC_E_ALIGN;
-  if (y == x || y == dy || dx == x || y == dx) return set_error(ACDC_E_SHAPE, "the fused step cannot write in place");
+  if (rows > 0 && (y == x || y == dy || dx == x || y == dx))
+    return set_error(ACDC_E_SHAPE, "the fused step cannot write in place");
   cudaStream_t st = (cudaStream_t)stream;
   if (rows == 0) {
     if (!accumulate) {

@@ -164,7 +164,7 @@ def acdc_step(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, d: torch.Tenso
     before the forward (AcdcLayer.forward then .backward, layers.py:141-156):
     returns (y, dx) and updates the gradients like :func:`acdc_backward`.
 
-    Up to :func:`step_max_rows` rows (small batches, 256 <= n <= 4096) this is
+    Up to :func:`step_max_rows` rows (small batches, 256 <= n <= 2048) this is
     ONE kernel launch (forward, backward and the gradient reduction in one
     CTA); larger batches run :func:`acdc_forward` + :func:`acdc_backward`."""
     n = a.shape[0]

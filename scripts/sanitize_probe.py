@@ -94,3 +94,19 @@ F.dct(rn(3, 4096))
 F.idct(rn(3, 4096))
 torch.cuda.synchronize()
 print("sanitize probe ok")
+
+
+# fused small-batch step: one cluster of CTAs, gradients over distributed shared memory
+def step(n, rows):
+    x, dy = rn(rows, n), rn(rows, n)
+    a, d, b = 1 + 0.1 * rn(n), 1 + 0.1 * rn(n), 0.1 * rn(n)
+    gr = torch.zeros(3, n, device=dev)
+    for _ in range(2):
+        F.acdc_step(x, dy, a, d, b, gr[0], gr[1], gr[2])
+
+
+step(256, 128)   # C1: 4 CTAs
+step(256, 1000)  # full cluster, several row pairs per group, ragged last pair
+step(4096, 9)    # one group per CTA
+torch.cuda.synchronize()
+print("sanitize probe: fused step done")
