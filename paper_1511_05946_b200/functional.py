@@ -12,6 +12,7 @@ Reference counterparts (under /root/reference/pkg/src/acdc):
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 
@@ -46,6 +47,16 @@ __all__ = [
     "relu_backward",
     "gather_cols",
 ]
+
+
+_NULLCTX = contextlib.nullcontext()
+
+
+def _on(dev: torch.device):
+    """Make ``dev`` current for the C call; no context switch (two cudaSetDevice
+    calls) when it already is -- the common case, and a measurable share of a
+    small call's host time."""
+    return _NULLCTX if dev.index is None or dev.index == torch.cuda.current_device() else torch.cuda.device(dev)
 
 
 def _ptr(t: torch.Tensor | None) -> int | None:
@@ -141,7 +152,7 @@ def acdc_forward(x: torch.Tensor, a: torch.Tensor, d: torch.Tensor, bias: torch.
     if h2cache is not None:
         _check_h2cache(h2cache, x.shape[0], n, dev)
     lib = _lib.load()
-    with torch.cuda.device(dev):
+    with _on(dev):
         if h2cache is None:
             rc = lib.acdc_fwd_f32(_ptr(x), _ptr(y), _ptr(a), _ptr(d), _ptr(bias), x.shape[0], n, _ld(x, n), _ld(y, n),
                                   _stream(x))
@@ -184,7 +195,7 @@ def acdc_step(x: torch.Tensor, dy: torch.Tensor, a: torch.Tensor, d: torch.Tenso
     y = torch.empty_like(x, memory_format=torch.contiguous_format) if out_y is None else _check_out(out_y, x, "out_y")
     dx = torch.empty_like(x, memory_format=torch.contiguous_format) if out_dx is None else _check_out(out_dx, x, "out_dx")
     lib = _lib.load()
-    with torch.cuda.device(dev):
+    with _on(dev):
         _lib.check(lib.acdc_step_f32(_ptr(x), _ptr(dy), _ptr(y), _ptr(dx), _ptr(a), _ptr(d), _ptr(bias), _ptr(grad_a),
                                      _ptr(grad_d), _ptr(grad_bias), 1 if accumulate else 0, rows, n, _ld(x, n),
                                      _ld(dy, n), _ld(y, n), _ld(dx, n), _stream(x)))
@@ -223,7 +234,7 @@ def acdc_backward(
     if h2cache is not None:
         _check_h2cache(h2cache, x.shape[0], n, dev)
     lib = _lib.load()
-    with torch.cuda.device(dev):
+    with _on(dev):
         wsb = lib.acdc_bwd_workspace_bytes(x.shape[0], n)
         if wsb == 0:
             _lib.check(_lib.ACDC_E_CUDA)
@@ -275,7 +286,7 @@ def acdc_backward_sgd(x, dy, params, velocities, lr, weight_decay, momentum, gra
     st.momentum = float(momentum)
     g = grads if grads is not None else (None, None, None)
     lib = _lib.load()
-    with torch.cuda.device(dev):
+    with _on(dev):
         wsb = lib.acdc_bwd_workspace_bytes(max(x.shape[0], 1), n)
         if wsb == 0:
             _lib.check(_lib.ACDC_E_CUDA)
@@ -424,7 +435,7 @@ def afdf_backward(x, dy, a, d, grad_a, grad_d, accumulate: bool = True, out=None
             raise ValueError("gradient buffers must be contiguous complex64 (n,) tensors on the input device")
     dx = torch.empty_like(x) if out is None else _check_out(out, x)
     lib = _lib.load()
-    with torch.cuda.device(dev):
+    with _on(dev):
         wsb = lib.afdf_bwd_workspace_bytes(x.shape[0], n)
         if wsb == 0:
             _lib.check(_lib.ACDC_E_SIZE if n > 16384 or n < 2 else _lib.ACDC_E_CUDA)
@@ -496,7 +507,7 @@ def cascade_forward(x: torch.Tensor, a: torch.Tensor, d: torch.Tensor, bias: tor
     y = torch.empty_like(x, memory_format=torch.contiguous_format) if out is None else _check_out(out, x)
     if x.shape[0] == 0:
         return y, ckpt
-    with torch.cuda.device(dev):
+    with _on(dev):
         if hl:  # ACDC-only stack on the half-length plan (x, y, params 16-byte aligned: _rows2d / contiguous)
             _lib.check(lib.cascade_fwd_hl_f32(_ptr(x), _ptr(y), depth, n, _ptr(a), _ptr(d), _ptr(bias), _ptr(ckpt),
                                               x.shape[0], _ld(x, n), _ld(y, n), _stream(x)))
@@ -562,7 +573,7 @@ def cascade_backward(x: torch.Tensor, dy: torch.Tensor, a, d, perm: torch.Tensor
     if tab is not None:
         return _cascade_backward_deferred(x, g, a, d, perm, fl, xs, h2, grads, tab, accumulate,
                                           perm_inv if gather else None, dstride)
-    with torch.cuda.device(dev):
+    with _on(dev):
         wsb = lib.acdc_bwd_workspace_bytes(rows, n)
         ws = torch.empty((wsb + 3) // 4, dtype=torch.float32, device=dev)
         for l in range(depth - 1, -1, -1):
@@ -616,7 +627,7 @@ def _cascade_backward_hl(x, g, a, d, xs, h2, grads, accumulate, sgd, on_block):
     lib = _lib.load()
     stride = lib.cascade_hl_defer_ws_bytes(rows, n) if (sgd is None and on_block is None) else 0
     tab = _grad_table(grads, dev) if stride else None
-    with torch.cuda.device(dev):
+    with _on(dev):
         if tab is not None:
             if any(t.shape != (n,) for gr in grads for t in gr):
                 raise ValueError("gradient buffers must be contiguous fp32 (n,) tensors on the input device")
@@ -679,7 +690,7 @@ def _cascade_backward_deferred(x, g, a, d, perm, fl, xs, h2, grads, tab, accumul
     has_perm = any(f & 2 for f in fl[:-1])
     pairs = (os.environ.get("ACDC_CASCADE_PAIR", "1") != "0" and depth >= 2 and (perm_inv is not None or not has_perm)
              and lib.cascade_pair_supported(rows, n) == 1)
-    with torch.cuda.device(dev):
+    with _on(dev):
         ws = torch.empty(depth * stride // 4, dtype=torch.float32, device=dev)
         l = depth - 1
         while pairs and l >= 1:  # blocks l (hi) and l-1 (lo) in one launch, the dx between them on chip
