@@ -674,6 +674,57 @@ __host__ __device__ constexpr bool step_ok() {
   // (n = 4096: 28.7 us fused vs 24.3 us separate at 8 rows -- the separate half-length kernels win)
   return G::FP && G::STASH_SMEM && G::GROUP_FLOATS >= 3 * G::N && !G::SPLIT && G::TW_SMEM && LOGN <= 11;
 }
+// The fused step's gradient epilogue: group partials -> the group's
+// shared-memory region; the CTA sums them in group order (fp64); CTA rank 0 of
+// the cluster adds the CTAs' sums in rank order over distributed shared memory
+// and writes the gradients (+= like the reference).
+template <class G>
+__device__ __forceinline__ void step_finish(const KParams& p, float* smem_f, float* gbase, const GroupSync<G>& gs,
+                                            const FastMap<G>& fm, const float2* st_ga2, const float (&acc_d)[16],
+                                            const float (&acc_b)[16]) {
+  constexpr int T = G::T;
+  constexpr int S = FastMap<G>::S;
+  float2 gav[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) gav[q] = st_ga2[q * T];
+  gs.sync();  // the group's stash is read before its region is reused
+  float* w = gbase;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    w[2 * (fm.jsp + q * S)] = gav[q].x;
+    w[2 * (fm.jsp + q * S) + 1] = gav[q].y;
+  }
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    *fm.plo(w + G::N, s) = acc_d[2 * s];
+    *fm.phi(w + G::N, s) = acc_d[2 * s + 1];
+    *fm.plo(w + 2 * G::N, s) = acc_b[2 * s];
+    *fm.phi(w + 2 * G::N, s) = acc_b[2 * s + 1];
+  }
+  __syncthreads();
+  float* csum = smem_f + G::TAB_FLOATS;  // group 0's region: the CTA's sums (each index read and written by one thread)
+  for (int i = threadIdx.x; i < 3 * G::N; i += blockDim.x) {
+    double acc = 0.0;
+#pragma unroll 4
+    for (int g = 0; g < G::GPC; ++g) acc += (double)csum[g * G::GROUP_FLOATS + i];
+    csum[i] = (float)acc;  // the per-CTA partial's rounding, as in the separate backward
+  }
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned ranks = cl.num_blocks();
+  if (ranks > 1) cl.sync();  // every CTA's sums are visible cluster-wide
+  if (cl.block_rank() == 0) {
+    for (int i = threadIdx.x; i < 3 * G::N; i += blockDim.x) {
+      double tot = 0.0;
+      for (unsigned r = 0; r < ranks; ++r) tot += (double)(r == 0 ? csum[i] : cl.map_shared_rank(csum, r)[i]);
+      const int comp = i / G::N, j = i - comp * G::N;
+      float* out = comp == 0 ? p.gout_a : (comp == 1 ? p.gout_d : p.gout_b);
+      if (p.accumulate) tot += (double)out[j];
+      out[j] = (float)tot;
+    }
+  }
+  if (ranks > 1) cl.sync();  // no CTA exits while rank 0 still reads its shared memory
+}
+
 // One cluster of up to 8 CTAs (one per SM): each CTA sums its groups' partials
 // (fp64, group order) into its group-0 region, then CTA rank 0 reads the other
 // CTAs' sums through distributed shared memory and adds them in rank order
@@ -839,47 +890,192 @@ __global__ void ACDC_LB(GeoStep<LOGN>) acdc_step_kernel(KParams p) {
       }
     }
   }
-  // group partials -> the group's shared-memory region; the CTA sums them in
-  // group order (fp64) and writes the gradients (+= like the reference)
-  float2 gav[8];
+  step_finish<G>(p, smem_f, gbase, gs, fm, st_ga2, acc_d, acc_b);
+}
+
+// Split-role fused step (T <= 32: N = 256, 512).  The step's per-thread
+// dependency chain (four 16-value transforms in a row) sets C1's time, so each
+// row pair goes to a PAIR of groups that run two transforms each, in parallel:
+// role 0 (even group) g3 = C2(dy) -> g1 = C3(d g3) -> dx, all gradients;
+// role 1 (odd group)  h2 = C2(a x) -> y = C3(d h2 + bias), publishing h2 to
+// role 0 through its stash (one pair barrier).  At T = 16 the pair is one warp
+// and both roles run the same transform code in lockstep on different data.
+// Per-element arithmetic is that of acdc_step_kernel.
+#ifndef ACDC_STEP2_CTA
+#define ACDC_STEP2_CTA 256
+#endif
+#ifndef ACDC_STEP_SPLIT  // 1: the split-role kernel where groups are at most one warp
+#define ACDC_STEP_SPLIT 1
+#endif
+template <int LOGN>
+using GeoStep2 = Geo<LOGN, 3 * Geo<LOGN>::E, (ACDC_STEP2_CTA / Geo<LOGN>::T > 1 ? ACDC_STEP2_CTA / Geo<LOGN>::T : 2)>;
+template <int LOGN>
+__host__ __device__ constexpr int step2_dstash_bytes() {
+  using G = GeoStep2<LOGN>;
+  return (G::FP && G::TW_SMEM && G::SMEM_BYTES + 8 * G::T * 16 <= G::SMEM_LIMIT) ? 8 * G::T * 16 : 0;
+}
+template <int LOGN>
+__host__ __device__ constexpr bool step2_ok() {
+  using G = GeoStep2<LOGN>;
+  return step_ok<LOGN>() && G::FP && G::T <= 32 && G::GPC % 2 == 0 && G::STASH_SMEM && G::GROUP_FLOATS >= 3 * G::N &&
+         G::TW_SMEM;
+}
+template <int LOGN>
+__global__ void ACDC_LB(GeoStep2<LOGN>) acdc_step2_kernel(KParams p) {
+  using G = GeoStep2<LOGN>;
+  static_assert(step2_ok<LOGN>(), "split-role step: groups of at most one warp, pairs of groups");
+  constexpr int E = G::E;
+  constexpr int T = G::T;
+  constexpr int S = FastMap<G>::S;
+  extern __shared__ __align__(16) float smem_f[];
+  const auto c = group_ctx<G>();
+  const int t = c.t;
+  const int role = c.grp & 1;
+  GroupSync<G> gs(c.grp);
+  float* gbase = smem_f + G::TAB_FLOATS + c.grp * G::GROUP_FLOATS;
+  Xbuf<G> xb{gbase, 0};
+  float* sbase = gbase + G::NBUF * G::BUF_FLOATS;
+  float4* st_h2 = reinterpret_cast<float4*>(sbase) + t;                               // role 1: h2 [slot][t]
+  const float4* pr_h2 = reinterpret_cast<const float4*>(sbase + G::GROUP_FLOATS) + t;  // role 0: the partner's
+  float2* st_ga2 = reinterpret_cast<float2*>(sbase + 2 * E * T) + t;                  // [8][T]: grad_a partials
+  constexpr bool DST = step2_dstash_bytes<LOGN>() > 0;
+  const float4* dst = reinterpret_cast<const float4*>(smem_f + G::SMEM_BYTES / 4) + t;
+  const FastMap<G> fm(t, gs.mask);
+  auto pair_sync = [&]() {
+    if constexpr (2 * T == 32) {
+      __syncwarp();  // the pair is the warp
+    } else if constexpr (2 * T < 32) {
+      const int lane = threadIdx.x & 31;
+      __syncwarp(((1u << (2 * T)) - 1u) << (lane & ~(2 * T - 1)));
+    } else {
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + (c.grp >> 1)), "r"(2 * T) : "memory");
+    }
+  };
+  const float2 *tw, *cp;
+  const int64_t npairs = (p.rows + 1) >> 1;
+  const int64_t pair0 = ((int64_t)blockIdx.x * G::GPC + c.grp) >> 1;
+  const int64_t pstride = ((int64_t)gridDim.x * G::GPC) >> 1;
+  pdl_wait();  // x, dy, a / d / bias may come from the previous kernel
+  float2 vin[16];  // this role's first input (dy, or a x), in flight across the table staging
+  auto load_in = [&](int64_t r) {
+    const int64_t r0 = 2 * r;
+    const bool hb = r0 + 1 < p.rows;
+    if (role)
+      fp_load<G, true>(vin, p.x + r0 * p.ldx, hb ? p.x + (r0 + 1) * p.ldx : nullptr, p.a, fm);
+    else
+      fp_load<G, false>(vin, p.dy + r0 * p.ldy, hb ? p.dy + (r0 + 1) * p.ldy : nullptr, nullptr, fm);
+  };
+  if (pair0 < npairs) load_in(pair0);
+  if constexpr (DST) {
+    if (c.grp == 0) {
 #pragma unroll
-  for (int q = 0; q < 8; ++q) gav[q] = st_ga2[q * T];
-  gs.sync();  // the group's stash is read before its region is reused
-  float* w = gbase;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    w[2 * (fm.jsp + q * S)] = gav[q].x;
-    w[2 * (fm.jsp + q * S) + 1] = gav[q].y;
-  }
-#pragma unroll
-  for (int s = 0; s < 8; ++s) {
-    *fm.plo(w + G::N, s) = acc_d[2 * s];
-    *fm.phi(w + G::N, s) = acc_d[2 * s + 1];
-    *fm.plo(w + 2 * G::N, s) = acc_b[2 * s];
-    *fm.phi(w + 2 * G::N, s) = acc_b[2 * s + 1];
-  }
-  __syncthreads();
-  float* csum = smem_f + G::TAB_FLOATS;  // group 0's region: the CTA's sums (each index read and written by one thread)
-  for (int i = threadIdx.x; i < 3 * G::N; i += blockDim.x) {
-    double acc = 0.0;
-#pragma unroll 4
-    for (int g = 0; g < G::GPC; ++g) acc += (double)csum[g * G::GROUP_FLOATS + i];
-    csum[i] = (float)acc;  // the per-CTA partial's rounding, as in the separate backward
-  }
-  cg::cluster_group cl = cg::this_cluster();
-  const unsigned ranks = cl.num_blocks();
-  if (ranks > 1) cl.sync();  // every CTA's sums are visible cluster-wide
-  if (cl.block_rank() == 0) {
-    for (int i = threadIdx.x; i < 3 * G::N; i += blockDim.x) {
-      double tot = 0.0;
-      for (unsigned r = 0; r < ranks; ++r) tot += (double)(r == 0 ? csum[i] : cl.map_shared_rank(csum, r)[i]);
-      const int comp = i / G::N, j = i - comp * G::N;
-      float* out = comp == 0 ? p.gout_a : (comp == 1 ? p.gout_d : p.gout_b);
-      if (p.accumulate) tot += (double)out[j];
-      out[j] = (float)tot;
+      for (int s = 0; s < 8; ++s)
+        reinterpret_cast<float4*>(smem_f + G::SMEM_BYTES / 4)[t + s * T] =
+            make_float4(__ldg(fm.plo(p.d, s)), __ldg(fm.phi(p.d, s)), __ldg(fm.plo(p.bias, s)),
+                        __ldg(fm.phi(p.bias, s)));
     }
   }
-  if (ranks > 1) cl.sync();  // no CTA exits while rank 0 still reads its shared memory
+  stage_tables<G>(p.tab, smem_f, tw, cp);
+  pdl_launch_dependents();
+  float acc_d[E], acc_b[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    acc_d[i] = acc_b[i] = 0.f;
+    if (i < E / 2) st_ga2[i * T] = make_float2(0.f, 0.f);
+  }
+  const float2 chi = tab_load<G>(cp, G::N / 2);
+  for (int64_t rp = pair0; rp < npairs; rp += pstride) {
+    const int64_t ra = 2 * rp;
+    const bool hasb = ra + 1 < p.rows;
+    const int64_t rb = hasb ? ra + 1 : ra;
+    float2 v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = vin[i];
+    if (rp + pstride < npairs) load_in(rp + pstride);
+    // role 0: g3 = C2(dy); role 1: h2 = C2(a x)
+    fft_passes<G, 0>(v, xb, gs, tw, t, fm.jsp, fm.jfq);
+    float2 zl[8], zh[8];
+    {
+      float2 w[8];
+      fp_partner<G>(v, w, fm);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) dct2_post(v[s], w[s], tab_load<G>(fm.plo(cp, s), 0), fm.special(s), chi, zl[s], zh[s]);
+    }
+    if (role) {
+#pragma unroll
+      for (int s = 0; s < 8; ++s) st_h2[s * T] = make_float4(zl[s].x, zl[s].y, zh[s].x, zh[s].y);
+    }
+    pair_sync();  // h2 published
+    if (!role) {  // grad_bias, grad_d partials (h2 from the partner)
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const float4 h = pr_h2[s * T];
+        acc_b[2 * s] += zl[s].x + zl[s].y;
+        acc_b[2 * s + 1] += zh[s].x + zh[s].y;
+        acc_d[2 * s] = fmaf(h.x, zl[s].x, fmaf(h.y, zl[s].y, acc_d[2 * s]));
+        acc_d[2 * s + 1] = fmaf(h.z, zh[s].x, fmaf(h.w, zh[s].y, acc_d[2 * s + 1]));
+      }
+    }
+    pair_sync();  // the partner's stash is free for the next row pair
+    // role 0: Y = d g3 (-> g1); role 1: d h2 + bias (-> y)
+    {
+      float2 gl[8], gh[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        const float2 cs = tab_load<G>(fm.plo(cp, s), 0);
+        float dl, dh, bl, bh;
+        if constexpr (DST) {
+          const float4 dv = dst[s * T];
+          dl = dv.x, dh = dv.y, bl = dv.z, bh = dv.w;
+        } else {
+          dl = ld_plain(fm.plo(p.d, s)), dh = ld_plain(fm.phi(p.d, s));
+          bl = ld_plain(fm.plo(p.bias, s)), bh = ld_plain(fm.phi(p.bias, s));
+        }
+        float2 ul, uh;
+        if (role) {
+          ul = vfma(zl[s], bc(dl), bc(bl));
+          uh = vfma(zh[s], bc(dh), bc(bh));
+        } else {
+          ul = vmul(bc(dl), zl[s]);
+          uh = vmul(bc(dh), zh[s]);
+        }
+        dct3_pre(ul, uh, cs, fm.special(s), chi, gl[s], gh[s]);
+      }
+      fp_scatter<G>(gl, gh, v, fm);
+    }
+    fft_passes<G, 0>(v, xb, gs, tw, t, fm.jfq, fm.jsp);
+    float2 oa[8], ob[8];
+    fp_out_pairs<G>(v, oa, ob, fm);
+    if (role) {  // y
+      float2* ya = reinterpret_cast<float2*>(p.yf + ra * p.ldyf + 2 * fm.jsp);
+      float2* yb = reinterpret_cast<float2*>(p.yf + rb * p.ldyf + 2 * fm.jsp);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        st_row_f2(ya + q * S, oa[q]);
+        if (hasb) st_row_f2(yb + q * S, ob[q]);
+      }
+    } else {  // dx = a g1; grad_a partial += x g1
+      float2* da = reinterpret_cast<float2*>(p.y + ra * p.ldo + 2 * fm.jsp);
+      float2* db = reinterpret_cast<float2*>(p.y + rb * p.ldo + 2 * fm.jsp);
+      const float* pxa = p.x + ra * p.ldx + 2 * fm.jsp;
+      const float* pxb = p.x + rb * p.ldx + 2 * fm.jsp;
+      const float* pa = p.a + 2 * fm.jsp;
+      float2 xav[8], xbv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        xav[q] = ld_row_f2(pxa + 2 * q * S);
+        xbv[q] = hasb ? ld_row_f2(pxb + 2 * q * S) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float2 av = ld_f2(pa + 2 * q * S);
+        st_ga2[q * T] = cadd(st_ga2[q * T], vfma(ob[q], xbv[q], vmul(oa[q], xav[q])));
+        st_row_f2(da + q * S, vmul(av, oa[q]));
+        if (hasb) st_row_f2(db + q * S, vmul(av, ob[q]));
+      }
+    }
+  }
+  step_finish<G>(p, smem_f, gbase, gs, fm, st_ga2, acc_d, acc_b);  // (role 1 contributes zeros)
 }
 
 // Cached-h2 backward with its per-thread gradient accumulators in TMEM
@@ -2064,6 +2260,19 @@ static int run(int kind, KParams p, int32_t n, cudaStream_t st) {
 template <int LOGN>
 static LaunchInfo step_info_t() {
   LaunchInfo li;
+#if ACDC_STEP_SPLIT
+  if constexpr (LOGN >= 8 && step2_ok<LOGN>()) {
+    using G = GeoStep2<LOGN>;
+    li.fn = (const void*)acdc_step2_kernel<LOGN>;
+    geom<G>(li, 0);
+    li.gpc = G::GPC / 2;  // row pairs per CTA and iteration (two groups per pair)
+    li.smem += step2_dstash_bytes<LOGN>();
+#ifndef ACDC_NO_PDL
+    li.pdl = true;
+#endif
+    return li;
+  }
+#endif
   if constexpr (LOGN >= 8 && step_ok<LOGN>()) {
     using G = GeoStep<LOGN>;
     li.fn = (const void*)acdc_step_kernel<LOGN>;
