@@ -130,8 +130,15 @@ template <int LOGN, int CTA>
 constexpr int fp_gpc() {
   return (CTA && Geo<LOGN>::FP && Geo<LOGN>::T <= CTA / 2) ? CTA / Geo<LOGN>::T : 0;
 }
+#ifndef ACDC_FWD_CTA_SMALL  // N = 256, 512: 1024-thread CTAs (64 registers) -- fewer waves over a 16384-row
+#define ACDC_FWD_CTA_SMALL 1024  // batch (N = 256: 1 instead of 1.15; 512: 1.73 instead of 2.31); forward
+#endif                           // 18.4 -> 12.3 / 34.8 -> 28.5 us, step -11% / -6% (A/B, profiles/round2/r2ad, r2ae)
 template <int LOGN>
-using GeoFwd = Geo<LOGN, 0, fp_gpc<LOGN, ACDC_FWD_CTA>()>;
+constexpr int fwd_cta() {
+  return (LOGN == 8 || LOGN == 9) ? ACDC_FWD_CTA_SMALL : ACDC_FWD_CTA;
+}
+template <int LOGN>
+using GeoFwd = Geo<LOGN, 0, fp_gpc<LOGN, fwd_cta<LOGN>()>()>;
 // Forward parameter stash: {d_lo, d_hi, b_lo, b_hi} of every thread's 8
 // spectral slots, [slot][t] float4s shared by the CTA's groups and filled once
 // per launch, so the slot pass reads one LDS.128 per slot instead of four
