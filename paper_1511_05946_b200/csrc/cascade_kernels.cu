@@ -23,6 +23,12 @@
 #endif
 namespace acdc {
 
+#ifndef ACDC_CASCADE_CTA  // threads per CTA of the fused cascade forward (0: the plan's 512)
+#define ACDC_CASCADE_CTA 0
+#endif
+template <int LOGN>
+using GeoC = Geo<LOGN, 0, (ACDC_CASCADE_CTA && ACDC_CASCADE_CTA / Geo<LOGN>::T > 1) ? ACDC_CASCADE_CTA / Geo<LOGN>::T : 0>;
+
 // d / bias of every block re-laid out per thread and slot, [block][slot][t]
 // float4 (d_lo, d_hi, b_lo, b_hi): the forward reads one coalesced 128-bit
 // value per slot and block instead of four scalar loads.
@@ -57,8 +63,8 @@ struct CParams {
 };
 
 template <int LOGN>
-__global__ void ACDC_LB(Geo<LOGN>) cascade_fwd_kernel(CParams p) {
-  using G = Geo<LOGN>;
+__global__ void ACDC_LB(GeoC<LOGN>) cascade_fwd_kernel(CParams p) {
+  using G = GeoC<LOGN>;
   static_assert(G::FP, "cascade fusion needs the fast-pairing path");
   pdl_launch_dependents();  // the last block's backward may stage its prologue while this grid drains
   constexpr int N = G::N, T = G::T, S = FastMap<G>::S;
@@ -190,7 +196,7 @@ __global__ void ACDC_LB(Geo<LOGN>) cascade_fwd_kernel(CParams p) {
 
 template <int LOGN>
 static LaunchInfo cinfo() {
-  using G = Geo<LOGN>;
+  using G = GeoC<LOGN>;
   LaunchInfo li;
   li.fn = (const void*)cascade_fwd_kernel<LOGN>;
   li.cta = G::CTA;
