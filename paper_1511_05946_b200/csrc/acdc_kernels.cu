@@ -2588,6 +2588,12 @@ int acdc_step_f32(const float* x, const float* dy, float* y, float* dx, const fl
   const int64_t npairs = (rows + 1) / 2;
   int64_t ctas = (npairs + li.gpc - 1) / li.gpc;
   if (ctas > ACDC_STEP_MAX_CLUSTER) ctas = ACDC_STEP_MAX_CLUSTER;
+#if ACDC_STEP_MAX_CLUSTER > 8
+  if (ctas > 8) {  // non-portable cluster size (opt-in)
+    cudaError_t ea = cudaFuncSetAttribute(li.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (ea != cudaSuccess) return set_cuda_error(ea);
+  }
+#endif
   void* args[] = {&p};
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[2];
